@@ -1,0 +1,331 @@
+"""Seeded graph / LP generators (torch; CPU for small cases, CUDA for full size).
+
+Recipes follow SURVEY.md §8(d) "Concrete synthetic inputs" and BASELINE.json
+configs (BJ:7-11).  The paper's own inputs (SuiteSparse graphs, Graph500 kron,
+rgg; Table 1) are not available; these synthetic graphs
+stand in for them (R-MAT with a,b,c,d = .57,.19,.19,.05 is the Graph500 recipe
+behind the paper's kron-X graphs).
+
+Every generator is deterministic for a given (seed, device type).  A CUDA- and
+a CPU-generated instance with the same seed differ; tests always take both
+sides' inputs from one generated instance.
+
+Edge-list conventions: edge id e = position in the returned list;
+general graphs store each undirected edge once with src < dst, lists sorted by
+(src, dst); bipartite graphs put left vertices at [0, n_left) and right
+vertices at [n_left, n_vertices), sorted by (left, right).
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import torch
+
+
+@dataclasses.dataclass
+class Graph:
+    src: torch.Tensor          # int32 [E]
+    dst: torch.Tensor          # int32 [E]
+    n_vertices: int
+    n_left: int = 0            # > 0: bipartite, left ids [0, n_left)
+    name: str = ""
+
+    @property
+    def n_edges(self) -> int:
+        return int(self.src.numel())
+
+    def to(self, device) -> "Graph":
+        return Graph(self.src.to(device), self.dst.to(device), self.n_vertices,
+                     self.n_left, self.name)
+
+    def numpy(self):
+        return self.src.cpu().numpy(), self.dst.cpu().numpy()
+
+
+@dataclasses.dataclass
+class CsrLP:
+    """A general positive LP  P x <= 1, C x >= 1, x >= 0  in CSR form (int64 rowptr)."""
+    n: int
+    p_rowptr: torch.Tensor | None
+    p_col: torch.Tensor | None
+    p_val: torch.Tensor | None
+    c_rowptr: torch.Tensor | None
+    c_col: torch.Tensor | None
+    c_val: torch.Tensor | None
+    name: str = ""
+
+
+def _gen(seed: int, device) -> torch.Generator:
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed))
+    return g
+
+
+def _finish(a: torch.Tensor, b: torch.Tensor, n: int, n_left: int, name: str) -> Graph:
+    return Graph(a.to(torch.int32).contiguous(), b.to(torch.int32).contiguous(), int(n), int(n_left), name)
+
+
+# --------------------------------------------------------------------------- c1
+def bipartite_uniform(n_left: int, n_right: int, n_edges: int, seed: int = 1, device="cpu") -> Graph:
+    """BJ:7 c1: n_edges distinct (left, right) pairs sampled uniformly without replacement.
+
+    key k drawn without replacement from [0, n_left*n_right); l = k // n_right,
+    r = n_left + k % n_right; sorted by (l, r).
+    """
+    g = _gen(seed, device)
+    total = n_left * n_right
+    if n_edges > total:
+        raise ValueError("more edges than pairs")
+    if total <= (1 << 26):
+        keys = torch.randperm(total, generator=g, device=device)[:n_edges]
+    else:  # rejection: oversample, dedup, random subset
+        keys = torch.empty(0, dtype=torch.int64, device=device)
+        while keys.numel() < n_edges:
+            k = int((n_edges - keys.numel()) * 1.2) + 1024
+            keys = torch.unique(torch.cat([keys, torch.randint(0, total, (k,), generator=g, device=device)]))
+        keys = keys[torch.randperm(keys.numel(), generator=g, device=device)[:n_edges]]
+    keys, _ = torch.sort(keys)
+    return _finish(keys // n_right, n_left + keys % n_right, n_left + n_right, n_left,
+                   f"bipartite_uniform({n_left}+{n_right},{n_edges})")
+
+
+# --------------------------------------------------------------------------- c2
+def erdos_renyi(n: int, m: int, seed: int = 1, device="cpu") -> Graph:
+    """BJ:8 c2: G(n, m) — m distinct unordered pairs u<v, no self-loops (rejection + dedup)."""
+    g = _gen(seed, device)
+    keys = torch.empty(0, dtype=torch.int64, device=device)
+    while keys.numel() < m:
+        k = int((m - keys.numel()) * 1.05) + 1024
+        u = torch.randint(0, n, (k,), generator=g, device=device, dtype=torch.int64)
+        v = torch.randint(0, n, (k,), generator=g, device=device, dtype=torch.int64)
+        keep = u != v
+        a, b = torch.minimum(u, v)[keep], torch.maximum(u, v)[keep]
+        keys = torch.unique(torch.cat([keys, a * n + b]))
+    if keys.numel() > m:
+        keys = keys[torch.randperm(keys.numel(), generator=g, device=device)[:m]]
+        keys, _ = torch.sort(keys)
+    return _finish(keys // n, keys % n, n, 0, f"erdos_renyi({n},{m})")
+
+
+# ------------------------------------------------------------------------ c3/c4
+def rmat(scale: int, edge_factor: int = 16, a=0.57, b=0.19, c=0.19, seed: int = 1, device="cpu",
+         chunk: int = 1 << 26) -> Graph:
+    """BJ:9/BJ:10 c3/c4: R-MAT (Graph500 recipe, no noise, no relabel), symmetrized,
+    self-loops dropped, duplicates removed.  edge_factor * 2^scale samples; per level
+    r < a -> (0,0), < a+b -> (0,1), < a+b+c -> (1,0), else (1,1)."""
+    g = _gen(seed, device)
+    n = 1 << scale
+    n_samples = edge_factor * n
+    keys = []
+    for start in range(0, n_samples, chunk):
+        k = min(chunk, n_samples - start)
+        u = torch.zeros(k, dtype=torch.int64, device=device)
+        v = torch.zeros(k, dtype=torch.int64, device=device)
+        for _ in range(scale):
+            r = torch.rand(k, generator=g, device=device, dtype=torch.float64)
+            bu = (r >= a + b).to(torch.int64)                              # quadrants (1,0),(1,1)
+            bv = ((r >= a) & (r < a + b)).to(torch.int64) | (r >= a + b + c).to(torch.int64)
+            u = u * 2 + bu
+            v = v * 2 + bv
+            del r, bu, bv
+        keep = u != v
+        lo, hi = torch.minimum(u, v)[keep], torch.maximum(u, v)[keep]
+        keys.append(torch.unique(lo * n + hi))
+        del u, v, keep, lo, hi
+    keys = torch.unique(torch.cat(keys))
+    return _finish(keys // n, keys % n, n, 0, f"rmat(s={scale},ef={edge_factor})")
+
+
+# --------------------------------------------------------------------------- c5
+def zipf_truncated_cap(s: float = 1.5, mean: float = 16.0) -> int:
+    """Smallest cap K with E[deg] >= mean for deg ~ Zipf(s) truncated to [1, K]."""
+    num = den = 0.0
+    k = 0
+    while True:
+        k += 1
+        w = k ** (-s)
+        num += k * w
+        den += w
+        if num / den >= mean:
+            return k
+
+
+def bipartite_zipf(n_left: int, n_right: int, n_edges: int, s: float = 1.5, seed: int = 1,
+                   device="cpu") -> Graph:
+    """BJ:11 c5 (reading SURVEY Q20): right-vertex degrees i.i.d. Zipf(s) truncated to [1, K]
+    with K the smallest cap giving mean >= n_edges/n_right, adjusted by +-1 on random right
+    vertices to total exactly n_edges; each right vertex gets distinct uniform left endpoints;
+    edges sorted by (left, right)."""
+    g = _gen(seed, device)
+    K = zipf_truncated_cap(s, n_edges / n_right)
+    ks = torch.arange(1, K + 1, dtype=torch.float64, device=device)
+    cdf = torch.cumsum(ks ** (-s), 0)
+    cdf = cdf / cdf[-1]
+    deg = torch.searchsorted(cdf, torch.rand(n_right, generator=g, device=device, dtype=torch.float64)) + 1
+    deg = deg.clamp_(1, K).to(torch.int64)
+    diff = n_edges - int(deg.sum())
+    while diff != 0:
+        elig = torch.nonzero(deg < min(K, n_left) if diff > 0 else deg > 1).flatten()
+        pick = elig[torch.randperm(elig.numel(), generator=g, device=device)[:abs(diff)]]
+        deg[pick] += 1 if diff > 0 else -1
+        diff = n_edges - int(deg.sum())
+    rights = torch.repeat_interleave(torch.arange(n_right, dtype=torch.int64, device=device), deg)
+    lefts = torch.randint(0, n_left, (n_edges,), generator=g, device=device, dtype=torch.int64)
+    while True:  # resample left endpoints that repeat within one right vertex
+        key = rights * n_left + lefts
+        skey, order = torch.sort(key)
+        dup_sorted = torch.zeros_like(skey, dtype=torch.bool)
+        dup_sorted[1:] = skey[1:] == skey[:-1]
+        ndup = int(dup_sorted.sum())
+        del skey, key
+        if ndup == 0:
+            del order, dup_sorted
+            break
+        idx = order[dup_sorted]
+        lefts[idx] = torch.randint(0, n_left, (ndup,), generator=g, device=device, dtype=torch.int64)
+        del order, dup_sorted, idx
+    key = lefts * n_right + rights
+    del lefts, rights
+    key, _ = torch.sort(key)
+    return _finish(key // n_right, n_left + key % n_right, n_left + n_right, n_left,
+                   f"bipartite_zipf({n_left}+{n_right},{n_edges},s={s})")
+
+
+# ------------------------------------------------------------- small families
+def _from_pairs(pairs, n, n_left=0, name="") -> Graph:
+    if len(pairs) == 0:
+        z = torch.zeros(0, dtype=torch.int32)
+        return Graph(z, z.clone(), n, n_left, name)
+    t = torch.tensor(sorted(tuple(p) for p in pairs), dtype=torch.int64)
+    return _finish(t[:, 0], t[:, 1], n, n_left, name)
+
+
+def complete_graph(n: int) -> Graph:
+    return _from_pairs([(i, j) for i in range(n) for j in range(i + 1, n)], n, 0, f"K{n}")
+
+
+def complete_bipartite(a: int, b: int) -> Graph:
+    return _from_pairs([(i, a + j) for i in range(a) for j in range(b)], a + b, a, f"K{a},{b}")
+
+
+def star_graph(leaves: int) -> Graph:
+    return _from_pairs([(0, j) for j in range(1, leaves + 1)], leaves + 1, 0, f"S{leaves}")
+
+
+def path_graph(n: int) -> Graph:
+    return _from_pairs([(i, i + 1) for i in range(n - 1)], n, 0, f"P{n}")
+
+
+def cycle_graph(n: int) -> Graph:
+    return _from_pairs([(min(i, (i + 1) % n), max(i, (i + 1) % n)) for i in range(n)], n, 0, f"C{n}")
+
+
+def circulant_regular(n: int, k: int) -> Graph:
+    """k-regular circulant graph on n vertices (k even: offsets 1..k/2; k odd needs n even: + n/2)."""
+    offs = list(range(1, k // 2 + 1))
+    pairs = set()
+    for i in range(n):
+        for o in offs:
+            j = (i + o) % n
+            pairs.add((min(i, j), max(i, j)))
+        if k % 2:
+            j = (i + n // 2) % n
+            pairs.add((min(i, j), max(i, j)))
+    return _from_pairs(sorted(pairs), n, 0, f"circ({n},{k})")
+
+
+def random_small_graph(n: int, p: float, seed: int) -> Graph:
+    g = _gen(seed, "cpu")
+    r = torch.rand(n, n, generator=g, dtype=torch.float64)
+    pairs = [(i, j) for i in range(n) for j in range(i + 1, n) if r[i, j] < p]
+    return _from_pairs(pairs, n, 0, f"gnp({n},{p},{seed})")
+
+
+def random_small_bipartite(a: int, b: int, p: float, seed: int) -> Graph:
+    g = _gen(seed, "cpu")
+    r = torch.rand(a, b, generator=g, dtype=torch.float64)
+    pairs = [(i, a + j) for i in range(a) for j in range(b) if r[i, j] < p]
+    return _from_pairs(pairs, a + b, a, f"bip({a},{b},{p},{seed})")
+
+
+# ---------------------------------------------------------- general CSR LPs
+def _random_csr(rows: int, n: int, density: float, g, lo=0.5, hi=2.0, min_per_row=1):
+    mask = torch.rand(rows, n, generator=g, dtype=torch.float64) < density
+    for r in range(rows):  # guarantee non-empty rows
+        if int(mask[r].sum()) < min_per_row:
+            mask[r, torch.randint(0, n, (min_per_row,), generator=g)] = True
+    vals = lo + (hi - lo) * torch.rand(rows, n, generator=g, dtype=torch.float64)
+    return torch.where(mask, vals, torch.zeros_like(vals))
+
+
+def _dense_to_csr(A: torch.Tensor):
+    rows, cols = torch.nonzero(A, as_tuple=True)
+    counts = torch.bincount(rows, minlength=A.shape[0])
+    rowptr = torch.zeros(A.shape[0] + 1, dtype=torch.int64)
+    rowptr[1:] = torch.cumsum(counts, 0)
+    return rowptr, cols.to(torch.int32), A[rows, cols].contiguous()
+
+
+def random_planted_lp(n: int, m_p: int, m_c: int, density: float, seed: int) -> CsrLP:
+    """Feasible-by-design positive LP (SPEC S:330 property suite): plant x* > 0, then
+    scale each packing row so (P x*)_j in [0.5, 1] and each covering row so (C x*)_j in [1, 2].
+    Every column of P gets a nonzero (P:272 init needs ||P_{:,i}||_inf > 0)."""
+    g = _gen(seed, "cpu")
+    xs = 0.5 + torch.rand(n, generator=g, dtype=torch.float64)
+    P = _random_csr(m_p, n, density, g)
+    for i in range(n):
+        if not bool((P[:, i] > 0).any()):
+            P[torch.randint(0, m_p, (1,), generator=g), i] = 1.0
+    C = _random_csr(m_c, n, density, g)
+    tp = 0.5 + 0.5 * torch.rand(m_p, generator=g, dtype=torch.float64)
+    tc = 1.0 + torch.rand(m_c, generator=g, dtype=torch.float64)
+    P = P * (tp / (P @ xs))[:, None]
+    C = C * (tc / (C @ xs))[:, None]
+    pr, pc, pv = _dense_to_csr(P)
+    cr, cc, cv = _dense_to_csr(C)
+    return CsrLP(n, pr, pc, pv, cr, cc, cv, f"planted({n},{m_p},{m_c},{seed})")
+
+
+def infeasible_lp(n: int, seed: int) -> CsrLP:
+    """Infeasible by construction: packing rows x_i <= 1/2 (P = 2I) and one covering row
+    (1/n) sum x >= 1 (needs mean x >= 1)."""
+    P = 2.0 * torch.eye(n, dtype=torch.float64)
+    C = torch.full((1, n), 1.0 / n, dtype=torch.float64)
+    pr, pc, pv = _dense_to_csr(P)
+    cr, cc, cv = _dense_to_csr(C)
+    return CsrLP(n, pr, pc, pv, cr, cc, cv, f"infeasible({n})")
+
+
+# ------------------------------------------------------------- BJ configs
+CONFIGS = {
+    # name: (kind, eps, description)                             BASELINE.json line
+    "c1": ("bmatch", 0.1, "bipartite uniform 1000+1000, 10,000 edges"),      # BJ:7
+    "c2": ("vcover", 0.05, "Erdos-Renyi n=2^20, avg degree 16"),              # BJ:8
+    "c3": ("domset", 0.05, "R-MAT scale 22, edge factor 16"),                 # BJ:9
+    "c4": ("densest", 0.1, "R-MAT scale 24, edge factor 16"),                 # BJ:10
+    "c5": ("bmatch", 0.1, "bipartite Zipf(1.5) 2^26+2^26, 2^30 edges"),      # BJ:11
+}
+
+
+def config_graph(name: str, scale_down: int = 0, seed: int = 1, device="cpu") -> Graph:
+    """The graph of config `name`; scale_down > 0 gives the same-recipe reduced instance
+    (vertex counts divided by 2^scale_down, average degree kept)."""
+    sd = int(scale_down)
+    if name == "c1":
+        return bipartite_uniform(1000, 1000, 10_000, seed=seed, device=device)
+    if name == "c2":
+        n = 1 << (20 - sd)
+        return erdos_renyi(n, 8 * n, seed=seed, device=device)
+    if name == "c3":
+        return rmat(22 - sd, 16, seed=seed, device=device)
+    if name == "c4":
+        return rmat(24 - sd, 16, seed=seed, device=device)
+    if name == "c5":
+        side = 1 << (26 - sd)
+        return bipartite_zipf(side, side, 16 * side, seed=seed, device=device)
+    raise KeyError(name)
+
+
+def _selfcheck():  # pragma: no cover - manual use
+    print(zipf_truncated_cap(1.5, 16.0), math.log(2))
