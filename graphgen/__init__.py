@@ -8,6 +8,6 @@ instances, small closed-form graph families and random positive LPs).  Both
 from .generators import (  # noqa: F401
     Graph, CsrLP, bipartite_uniform, erdos_renyi, rmat, bipartite_zipf,
     complete_graph, complete_bipartite, star_graph, path_graph, cycle_graph,
-    circulant_regular, random_small_graph, random_small_bipartite,
+    circulant_regular, random_small_graph, hub_graph, random_small_bipartite,
     random_planted_lp, infeasible_lp, config_graph, CONFIGS,
 )

@@ -249,6 +249,24 @@ def random_small_bipartite(a: int, b: int, p: float, seed: int) -> Graph:
     return _from_pairs(pairs, a + b, a, f"bip({a},{b},{p},{seed})")
 
 
+def hub_graph(n: int, hubs: int, hub_deg: int, extra: int, seed: int = 1) -> Graph:
+    """Graph with `hubs` vertices of degree >= hub_deg (long rows, > one seg tile) plus `extra`
+    random edges; exercises the long-row path of the segmented kernels."""
+    g = _gen(seed, "cpu")
+    keys = []
+    for h in range(hubs):
+        nb = torch.randperm(n, generator=g)[:hub_deg + 1]
+        nb = nb[nb != h][:hub_deg]
+        a, b = torch.minimum(nb, torch.tensor(h)), torch.maximum(nb, torch.tensor(h))
+        keys.append(a * n + b)
+    u = torch.randint(0, n, (extra,), generator=g)
+    v = torch.randint(0, n, (extra,), generator=g)
+    keep = u != v
+    keys.append(torch.minimum(u, v)[keep] * n + torch.maximum(u, v)[keep])
+    k = torch.unique(torch.cat(keys))
+    return _finish(k // n, k % n, n, 0, f"hub({n},{hubs},{hub_deg},{extra})")
+
+
 # ---------------------------------------------------------- general CSR LPs
 def _random_csr(rows: int, n: int, density: float, g, lo=0.5, hi=2.0, min_per_row=1):
     mask = torch.rand(rows, n, generator=g, dtype=torch.float64) < density

@@ -222,7 +222,8 @@ def direction(g, h, x, sigma: float) -> np.ndarray:
     x = np.asarray(x, dtype=np.float64)
     d = np.zeros_like(x)
     pos = h > 0
-    d[pos] = sigma * np.maximum(0.0, 1.0 - g[pos] / h[pos]) * x[pos]
+    with np.errstate(over="ignore"):     # g/h = inf where h underflowed: clipped to 0 below
+        d[pos] = sigma * np.maximum(0.0, 1.0 - g[pos] / h[pos]) * x[pos]
     return d
 
 
@@ -350,7 +351,7 @@ class Probe:
     step() so tests can run it in lockstep with the GPU (T3 fixed-step parity)."""
 
     def __init__(self, lp: LP, eps: float, max_iter: int = 5000, eta_factor: float = 10.0,
-                 tol_mode: str = "prose", max_evals: int = 200):
+                 tol_mode: str = "prose", max_evals: int = 200, x0_scale: float = 1.0):
         self.lp, self.eps, self.max_iter = lp, eps, max_iter
         self.tol_mode, self.max_evals = tol_mode, max_evals
         self.P, self.C = lp.P, lp.C
@@ -364,6 +365,8 @@ class Probe:
         if lp.C.shape[0] > 0 and np.any(np.diff(lp.C.indptr) == 0):
             self.status, self.reason = INFEASIBLE, "EMPTY_COVER_ROW"    # Q17: 0 >= 1 fails
         self.x = init_x(lp.P, eps)
+        if x0_scale != 1.0:   # test knob: one-ulp perturbation to measure fp sensitivity
+            self.x = self.x * x0_scale
         self.y = self.P @ self.x
         self.z = self.C @ self.x
         self._weights()
@@ -494,12 +497,13 @@ class SolveResult:
 def solve(kind: str, src=None, dst=None, n_vertices: int = 0, eps: float = 0.1,
           max_iter: int = 5000, P: sp.csr_matrix | None = None, C: sp.csr_matrix | None = None,
           tol_mode: str = "prose", max_evals: int = 200, eta_factor: float = 10.0,
-          outer_rel_tol: float | None = None) -> SolveResult:
+          outer_rel_tol: float | None = None, x0_scale: float = 1.0) -> SolveResult:
     """Full solve: outer geometric bisection (Q14) over M (pure modes) or D (densest) with a
     fresh Alg. 2 probe per bound; IterLimit counts as infeasible.  kind in {bmatch, match,
     vcover, domset, densest, packing, covering, mixed}; the last three take explicit P / C."""
     rt = eps / 4.0 if outer_rel_tol is None else outer_rel_tol
-    kw = dict(max_iter=max_iter, eta_factor=eta_factor, tol_mode=tol_mode, max_evals=max_evals)
+    kw = dict(max_iter=max_iter, eta_factor=eta_factor, tol_mode=tol_mode, max_evals=max_evals,
+              x0_scale=x0_scale)
     if kind == "mixed":
         p = run_probe(mixed_lp(P, C), eps, **kw)
         ok = p.status == FEASIBLE

@@ -1,0 +1,1312 @@
+// mwu.cu — context, structure build, probe engine (host-driven or one CUDA-graph launch per
+// probe via conditional WHILE nodes), outer bisection and the C ABI of include/mwu.h.
+#include "../../include/mwu.h"
+#include "kernels.cuh"
+#include "storage.cuh"
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+using namespace mwu;
+
+namespace {
+
+thread_local std::string g_create_err;
+
+enum Kind { K_CSR = 0, K_MATCH = 1, K_VCOVER = 2, K_DOMSET = 3, K_DENSEST = 4 };
+
+struct MwuError {
+  mwu_status st;
+  std::string msg;
+};
+
+#define CK(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      throw MwuError{e_ == cudaErrorMemoryAllocation ? MWU_ERR_OOM : MWU_ERR_CUDA,                 \
+                     std::string(#call) + ": " + cudaGetErrorString(e_)};                          \
+  } while (0)
+#define CKL() CK(cudaGetLastError())
+
+struct Seg {
+  int64_t nrows = 0, nnz = 0;
+  int64_t* rowptr = nullptr;
+  uint32_t* idx = nullptr;
+  double* val = nullptr;
+  int64_t ntiles = 0;
+  int64_t* tile_row = nullptr;
+  int64_t nlong = 0, nchunks = 0;
+  int64_t* long_rows = nullptr;
+  int64_t* long_cptr = nullptr;
+  double* chunk_sum = nullptr;
+  SegView view() const {
+    SegView s;
+    s.rowptr = rowptr; s.nrows = nrows; s.idx = idx; s.val = val; s.tile_row = tile_row; s.ntiles = ntiles;
+    s.long_rows = long_rows; s.long_cptr = long_cptr; s.nlong = nlong; s.nchunks = nchunks; s.chunk_sum = chunk_sum;
+    return s;
+  }
+};
+
+}  // namespace
+
+struct mwu_ctx {
+  mwu_options opt{};
+  int dev = 0;
+  cudaStream_t st = nullptr;
+  std::string err;
+  bool poisoned = false;
+  int kind = K_CSR, mode = MWU_MIXED;
+  int64_t n = 0, nv = 0, E = 0, nleft = 0;
+  int64_t mP = 0, mC = 0;
+  int pSing = 0, cSing = 0;
+  int64_t nnzP = 0, nnzC = 0, empty_dropped = 0;
+  bool empty_cover = false;
+  // graph storage
+  int32_t *src = nullptr, *dst = nullptr, *srow = nullptr, *drow = nullptr, *deg = nullptr, *prow = nullptr;
+  Seg inc_all, inc_p;
+  int64_t maxdeg = 0, nprime = 0;
+  // CSR storage
+  Seg csrP, cscP, csrC, cscC;
+  double *colmaxP = nullptr, *colsumC = nullptr, *crecipC = nullptr, *crecipP = nullptr;
+  // vectors
+  double *x = nullptr, *d = nullptr, *y = nullptr, *dy = nullptr, *u = nullptr, *z = nullptr, *dz = nullptr,
+         *v = nullptr, *gtmp = nullptr, *gdbg = nullptr, *hdbg = nullptr, *xbest = nullptr, *tmp = nullptr;
+  Ctl* ctl = nullptr;
+  Ctl* hctl = nullptr;  // pinned host mirror
+  double* part = nullptr;
+  unsigned int* counter = nullptr;
+  int sms = 148, grid_rows = 592, grid_max = 1184;
+  std::vector<void*> allocs;
+  bool probe_active = false;
+  double bound = 0, eps = 0;
+  int record = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  unsigned long long h_iter = 0, h_search = 0;
+  bool graph_ok = false;
+  mwu_stats stats{};
+  int64_t launches = 0;
+  double bytes_alg = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+// ------------------------------------------------------------------------------ memory
+template <class T>
+T* dalloc(mwu_ctx* c, int64_t n) {
+  if (n <= 0) n = 1;
+  void* p = nullptr;
+  CK(cudaMalloc(&p, (size_t)n * sizeof(T)));
+  c->allocs.push_back(p);
+  return (T*)p;
+}
+template <class T>
+T* talloc(int64_t n) {  // temporary (caller frees with tfree)
+  if (n <= 0) n = 1;
+  void* p = nullptr;
+  CK(cudaMalloc(&p, (size_t)n * sizeof(T)));
+  return (T*)p;
+}
+void tfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+int grid_for(mwu_ctx* c, int64_t n) {
+  int64_t g = (n + MWU_NT - 1) / MWU_NT;
+  if (g < 1) g = 1;
+  if (g > c->grid_max) g = c->grid_max;
+  return (int)g;
+}
+
+int bits_for(int64_t n) {
+  int b = 1;
+  while (b < 63 && (int64_t(1) << b) < n) ++b;
+  return b;
+}
+
+void sync(mwu_ctx* c) { CK(cudaStreamSynchronize(c->st)); }
+
+template <class T>
+T read_scalar(mwu_ctx* c, const T* dptr) {
+  T h;
+  CK(cudaMemcpyAsync(&h, dptr, sizeof(T), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  return h;
+}
+
+void pull_ctl(mwu_ctx* c) {
+  CK(cudaMemcpyAsync(c->hctl, c->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+}
+
+template <class T>
+void push_field(mwu_ctx* c, T* dfield, T val) {
+  CK(cudaMemcpyAsync(dfield, &val, sizeof(T), cudaMemcpyHostToDevice, c->st));
+  sync(c);  // val is a stack value
+}
+
+// exclusive scan of n int64 values into out[n+1] (out[n] = total)
+void exclusive_scan_total(mwu_ctx* c, const int64_t* in_n, int64_t* out, int64_t n) {
+  int64_t* tmp = talloc<int64_t>(n + 1);
+  CK(cudaMemsetAsync(tmp + n, 0, sizeof(int64_t), c->st));
+  if (n > 0) CK(cudaMemcpyAsync(tmp, in_n, n * sizeof(int64_t), cudaMemcpyDeviceToDevice, c->st));
+  size_t tb = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, tmp, out, n + 1, c->st));
+  void* t = talloc<char>(tb);
+  CK(cub::DeviceScan::ExclusiveSum(t, tb, tmp, out, n + 1, c->st));
+  sync(c);
+  tfree(t);
+  tfree(tmp);
+}
+
+// tile plan + long rows of a segmented structure
+void build_plan(mwu_ctx* c, Seg& s) {
+  s.ntiles = s.nnz / MWU_TILE + 1;
+  s.tile_row = dalloc<int64_t>(c, s.ntiles + 1);
+  k_tile_rows<<<grid_for(c, s.ntiles + 1), MWU_NT, 0, c->st>>>(s.rowptr, s.nrows, s.ntiles, s.tile_row);
+  CKL();
+  if (s.nrows == 0) return;
+  uint8_t* flags = talloc<uint8_t>(s.nrows);
+  k_long_flags<<<grid_for(c, s.nrows), MWU_NT, 0, c->st>>>(s.rowptr, s.nrows, flags);
+  CKL();
+  int64_t* sel = talloc<int64_t>(s.nrows);
+  int64_t* nsel = talloc<int64_t>(1);
+  cub::CountingInputIterator<int64_t> it(0);
+  size_t tb = 0;
+  CK(cub::DeviceSelect::Flagged(nullptr, tb, it, flags, sel, nsel, s.nrows, c->st));
+  void* t = talloc<char>(tb);
+  CK(cub::DeviceSelect::Flagged(t, tb, it, flags, sel, nsel, s.nrows, c->st));
+  s.nlong = read_scalar(c, nsel);
+  tfree(t);
+  if (s.nlong > 0) {
+    s.long_rows = dalloc<int64_t>(c, s.nlong);
+    CK(cudaMemcpyAsync(s.long_rows, sel, s.nlong * sizeof(int64_t), cudaMemcpyDeviceToDevice, c->st));
+    int64_t* nch = talloc<int64_t>(s.nlong);
+    k_long_nchunks<<<grid_for(c, s.nlong), MWU_NT, 0, c->st>>>(s.rowptr, s.long_rows, s.nlong, nch);
+    CKL();
+    s.long_cptr = dalloc<int64_t>(c, s.nlong + 1);
+    exclusive_scan_total(c, nch, s.long_cptr, s.nlong);
+    s.nchunks = read_scalar(c, s.long_cptr + s.nlong);
+    s.chunk_sum = dalloc<double>(c, s.nchunks);
+    tfree(nch);
+  }
+  sync(c);
+  tfree(sel);
+  tfree(nsel);
+  tfree(flags);
+}
+
+// CSC copy of a CSR (rows x cols): stable sort of entries by column keeps rows ascending.
+void build_csc(mwu_ctx* c, const Seg& A, int64_t cols, Seg& T) {
+  T.nrows = cols;
+  T.nnz = A.nnz;
+  T.rowptr = dalloc<int64_t>(c, cols + 1);
+  T.idx = dalloc<uint32_t>(c, A.nnz);
+  T.val = A.val ? dalloc<double>(c, A.nnz) : nullptr;
+  if (A.nnz > 0) {
+    uint32_t* rid = talloc<uint32_t>(A.nnz);
+    k_row_ids<<<grid_for(c, A.nrows), MWU_NT, 0, c->st>>>(A.nrows, A.rowptr, rid);
+    CKL();
+    uint32_t* kout = talloc<uint32_t>(A.nnz);
+    uint64_t* vin = talloc<uint64_t>(A.nnz);
+    uint64_t* vout = talloc<uint64_t>(A.nnz);
+    k_iota64<<<grid_for(c, A.nnz), MWU_NT, 0, c->st>>>(A.nnz, vin);
+    CKL();
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, A.idx, kout, vin, vout, A.nnz, 0, bits_for(cols + 1), c->st));
+    void* t = talloc<char>(tb);
+    CK(cub::DeviceRadixSort::SortPairs(t, tb, A.idx, kout, vin, vout, A.nnz, 0, bits_for(cols + 1), c->st));
+    k_gather_csc<<<grid_for(c, A.nnz), MWU_NT, 0, c->st>>>(A.nnz, vout, rid, A.val, T.idx, T.val);
+    CKL();
+    int64_t* cnt = talloc<int64_t>(cols);
+    CK(cudaMemsetAsync(cnt, 0, cols * sizeof(int64_t), c->st));
+    k_col_count<<<grid_for(c, A.nnz), MWU_NT, 0, c->st>>>(A.nnz, A.idx, cnt);
+    CKL();
+    exclusive_scan_total(c, cnt, T.rowptr, cols);
+    sync(c);
+    tfree(t); tfree(rid); tfree(kout); tfree(vin); tfree(vout); tfree(cnt);
+  } else {
+    CK(cudaMemsetAsync(T.rowptr, 0, (cols + 1) * sizeof(int64_t), c->st));
+  }
+  build_plan(c, T);
+}
+
+double rp_bytes(int64_t nnz) { return nnz < (int64_t(1) << 31) ? 4.0 : 8.0; }
+
+void alloc_vectors(mwu_ctx* c) {
+  c->x = dalloc<double>(c, c->n);
+  c->d = dalloc<double>(c, c->n);
+  c->xbest = dalloc<double>(c, c->n);
+  c->y = dalloc<double>(c, c->mP);
+  c->dy = dalloc<double>(c, c->mP);
+  c->u = dalloc<double>(c, c->mP);
+  c->z = dalloc<double>(c, c->mC);
+  c->dz = dalloc<double>(c, c->mC);
+  c->v = dalloc<double>(c, c->mC);
+  int64_t mx = c->n;
+  if (c->mP > mx) mx = c->mP;
+  if (c->mC > mx) mx = c->mC;
+  c->tmp = dalloc<double>(c, mx);
+  if (c->kind == K_CSR && !c->pSing && !c->cSing) c->gtmp = dalloc<double>(c, c->n);
+  CK(cudaMemsetAsync(c->d, 0, c->n * sizeof(double), c->st));
+  CK(cudaMemsetAsync(c->x, 0, c->n * sizeof(double), c->st));
+  CK(cudaMemsetAsync(c->xbest, 0, c->n * sizeof(double), c->st));
+  CK(cudaMemsetAsync(c->dy, 0, (c->mP > 0 ? c->mP : 1) * sizeof(double), c->st));
+  CK(cudaMemsetAsync(c->dz, 0, (c->mC > 0 ? c->mC : 1) * sizeof(double), c->st));
+}
+
+void init_ctx_common(mwu_ctx* c, const mwu_options* opt) {
+  if (opt) c->opt = *opt; else mwu_default_options(&c->opt);
+  if (c->opt.device >= 0) CK(cudaSetDevice(c->opt.device));
+  CK(cudaGetDevice(&c->dev));
+  CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->dev));
+  c->grid_rows = c->sms * 4;
+  c->grid_max = c->sms * 8;
+  CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+  c->ctl = dalloc<Ctl>(c, 1);
+  CK(cudaMallocHost(&c->hctl, sizeof(Ctl)));
+  memset(c->hctl, 0, sizeof(Ctl));
+  CK(cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st));
+  c->part = dalloc<double>(c, (int64_t)c->grid_max * MWU_SLOTS);
+  c->counter = dalloc<unsigned int>(c, 1);
+  CK(cudaMemsetAsync(c->counter, 0, sizeof(unsigned int), c->st));
+  CK(cudaEventCreate(&c->ev0));
+  CK(cudaEventCreate(&c->ev1));
+}
+
+// ------------------------------------------------------------------------------ graph build
+void build_graph_storage(mwu_ctx* c, const mwu_graph* g) {
+  const int64_t E = g->n_edges, nv = g->n_vertices;
+  c->E = E; c->nv = nv; c->nleft = g->n_left;
+  c->src = dalloc<int32_t>(c, E);
+  c->dst = dalloc<int32_t>(c, E);
+  if (E > 0) {
+    CK(cudaMemcpyAsync(c->src, g->src, E * sizeof(int32_t), cudaMemcpyDefault, c->st));
+    CK(cudaMemcpyAsync(c->dst, g->dst, E * sizeof(int32_t), cudaMemcpyDefault, c->st));
+  }
+  // validation: range, self-loops, bipartite sides, duplicate edges
+  unsigned int* err = talloc<unsigned int>(1);
+  CK(cudaMemsetAsync(err, 0, sizeof(unsigned int), c->st));
+  if (E > 0) {
+    unsigned long long* keys = talloc<unsigned long long>(E);
+    unsigned long long* keys2 = talloc<unsigned long long>(E);
+    k_validate_edges<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->src, c->dst, nv, g->n_left,
+                                                            g->kind == MWU_G_BMATCH && g->n_left > 0, err, keys);
+    CKL();
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, keys2, E, 0, 64, c->st));
+    void* t = talloc<char>(tb);
+    CK(cub::DeviceRadixSort::SortKeys(t, tb, keys, keys2, E, 0, 64, c->st));
+    k_adjacent_dups<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, keys2, err);
+    CKL();
+    sync(c);
+    tfree(t); tfree(keys); tfree(keys2);
+  }
+  const unsigned int ebits = read_scalar(c, err);
+  tfree(err);
+  if (ebits) {
+    std::string m = "invalid graph:";
+    if (ebits & 1) m += " vertex id out of range;";
+    if (ebits & 2) m += " self-loop;";
+    if (ebits & 4) m += " BMATCH edge not between the two sides split at n_left;";
+    if (ebits & 8) m += " duplicate edge;";
+    throw MwuError{MWU_ERR_ARG, m};
+  }
+  // degrees
+  c->deg = dalloc<int32_t>(c, nv);
+  CK(cudaMemsetAsync(c->deg, 0, nv * sizeof(int32_t), c->st));
+  if (E > 0) { k_degree<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->src, c->dst, c->deg); CKL(); }
+  {
+    int64_t* deg64 = talloc<int64_t>(nv);
+    k_to_int64<int32_t><<<grid_for(c, nv), MWU_NT, 0, c->st>>>(nv, c->deg, deg64, 0);
+    CKL();
+    int64_t* outm = talloc<int64_t>(1);
+    size_t tb = 0;
+    CK(cub::DeviceReduce::Max(nullptr, tb, deg64, outm, nv, c->st));
+    void* t = talloc<char>(tb);
+    CK(cub::DeviceReduce::Max(t, tb, deg64, outm, nv, c->st));
+    c->maxdeg = read_scalar(c, outm);
+    tfree(t);
+    // incidence CSR over all vertices (rowptr = exclusive scan of deg)
+    if (g->kind != MWU_G_DOMSET) {
+      c->inc_all.nrows = nv;
+      c->inc_all.nnz = 2 * E;
+      c->inc_all.rowptr = dalloc<int64_t>(c, nv + 1);
+      exclusive_scan_total(c, deg64, c->inc_all.rowptr, nv);
+    }
+    // non-isolated vertex count n'
+    int64_t* fl = talloc<int64_t>(nv);
+    k_nonzero_flags<<<grid_for(c, nv), MWU_NT, 0, c->st>>>(nv, c->deg, fl);
+    CKL();
+    int64_t* scan = talloc<int64_t>(nv + 1);
+    exclusive_scan_total(c, fl, scan, nv);
+    c->nprime = read_scalar(c, scan + nv);
+    if (g->kind == MWU_G_MATCH || g->kind == MWU_G_BMATCH || g->kind == MWU_G_DENSEST) {
+      c->prow = dalloc<int32_t>(c, nv);
+      c->inc_p.nrows = c->nprime;
+      c->inc_p.nnz = 2 * E;
+      c->inc_p.rowptr = dalloc<int64_t>(c, c->nprime + 1);
+    }
+    // slots sorted by vertex (stable radix sort keeps slot order within a vertex)
+    if (g->kind != MWU_G_DOMSET) {
+      c->inc_all.idx = dalloc<uint32_t>(c, 2 * E);
+      if (E > 0) {
+        uint32_t *keys = talloc<uint32_t>(2 * E), *kout = talloc<uint32_t>(2 * E), *vals = talloc<uint32_t>(2 * E);
+        k_slot_keys<<<grid_for(c, 2 * E), MWU_NT, 0, c->st>>>(E, c->src, c->dst, keys, vals);
+        CKL();
+        size_t tb2 = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, keys, kout, vals, c->inc_all.idx, 2 * E, 0, bits_for(nv + 1), c->st));
+        void* t2 = talloc<char>(tb2);
+        CK(cub::DeviceRadixSort::SortPairs(t2, tb2, keys, kout, vals, c->inc_all.idx, 2 * E, 0, bits_for(nv + 1), c->st));
+        sync(c);
+        tfree(t2); tfree(keys); tfree(kout); tfree(vals);
+      }
+    }
+    if (c->prow) {
+      k_compact_rows<<<grid_for(c, nv), MWU_NT, 0, c->st>>>(nv, c->deg, scan, c->inc_all.rowptr, c->prow, c->inc_p.rowptr);
+      CKL();
+      const int64_t tot = 2 * E;
+      CK(cudaMemcpyAsync(c->inc_p.rowptr + c->nprime, &tot, sizeof(int64_t), cudaMemcpyHostToDevice, c->st));
+      c->inc_p.idx = c->inc_all.idx;
+      c->srow = dalloc<int32_t>(c, E);
+      c->drow = dalloc<int32_t>(c, E);
+      if (E > 0) { k_map_endpoints<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->src, c->dst, c->prow, c->srow, c->drow); CKL(); }
+      sync(c);
+    }
+    sync(c);
+    tfree(deg64); tfree(outm); tfree(fl); tfree(scan);
+  }
+  if (g->kind == MWU_G_DOMSET) {
+    // C = I + A as CSR: sort (row << 32 | col) keys of diagonal and both edge directions
+    const int64_t tot = nv + 2 * E;
+    unsigned long long *keys = talloc<unsigned long long>(tot), *kout = talloc<unsigned long long>(tot);
+    k_domset_keys<<<grid_for(c, tot), MWU_NT, 0, c->st>>>(nv, E, c->src, c->dst, keys);
+    CKL();
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, kout, tot, 0, 64, c->st));
+    void* t = talloc<char>(tb);
+    CK(cub::DeviceRadixSort::SortKeys(t, tb, keys, kout, tot, 0, 64, c->st));
+    c->csrC.nrows = nv;
+    c->csrC.nnz = tot;
+    c->csrC.idx = dalloc<uint32_t>(c, tot);
+    k_low32<<<grid_for(c, tot), MWU_NT, 0, c->st>>>(tot, kout, c->csrC.idx);
+    CKL();
+    int64_t* deg1 = talloc<int64_t>(nv);
+    k_to_int64<int32_t><<<grid_for(c, nv), MWU_NT, 0, c->st>>>(nv, c->deg, deg1, 1);
+    CKL();
+    c->csrC.rowptr = dalloc<int64_t>(c, nv + 1);
+    exclusive_scan_total(c, deg1, c->csrC.rowptr, nv);
+    sync(c);
+    tfree(t); tfree(keys); tfree(kout); tfree(deg1);
+    build_plan(c, c->csrC);
+    c->cscC = c->csrC;  // symmetric: the CSR doubles as the CSC (column side)
+    c->nnzC = tot;
+  }
+  if (c->inc_p.rowptr) build_plan(c, c->inc_p);
+  if (g->kind == MWU_G_VCOVER) build_plan(c, c->inc_all);
+}
+
+// ------------------------------------------------------------------------------ CSR build
+void copy_csr_checked(mwu_ctx* c, const mwu_csr* A, Seg& S, int64_t cols, const char* name) {
+  if (A->rows < 0 || A->cols != cols || A->nnz < 0 || !A->rowptr || (A->nnz > 0 && !A->colidx))
+    throw MwuError{MWU_ERR_ARG, std::string(name) + ": bad dimensions or null pointers"};
+  S.nrows = A->rows;
+  S.nnz = A->nnz;
+  S.rowptr = dalloc<int64_t>(c, A->rows + 1);
+  S.idx = dalloc<uint32_t>(c, A->nnz);
+  CK(cudaMemcpyAsync(S.rowptr, A->rowptr, (A->rows + 1) * sizeof(int64_t), cudaMemcpyDefault, c->st));
+  if (A->nnz > 0) CK(cudaMemcpyAsync(S.idx, A->colidx, A->nnz * sizeof(int32_t), cudaMemcpyDefault, c->st));
+  if (A->vals) {
+    S.val = dalloc<double>(c, A->nnz);
+    if (A->nnz > 0) CK(cudaMemcpyAsync(S.val, A->vals, A->nnz * sizeof(double), cudaMemcpyDefault, c->st));
+  }
+  int64_t ends[2];
+  CK(cudaMemcpyAsync(&ends[0], S.rowptr, sizeof(int64_t), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaMemcpyAsync(&ends[1], S.rowptr + A->rows, sizeof(int64_t), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  if (ends[0] != 0 || ends[1] != A->nnz) throw MwuError{MWU_ERR_ARG, std::string(name) + ": rowptr[0] != 0 or rowptr[rows] != nnz"};
+  unsigned int* err = talloc<unsigned int>(1);
+  int32_t* rl = talloc<int32_t>(A->rows);
+  CK(cudaMemsetAsync(err, 0, sizeof(unsigned int), c->st));
+  if (A->rows > 0) { k_validate_csr<<<grid_for(c, A->rows), MWU_NT, 0, c->st>>>(A->rows, cols, S.rowptr, S.idx, S.val, err, rl); CKL(); }
+  const unsigned int eb = read_scalar(c, err);
+  tfree(err);
+  tfree(rl);
+  if (eb & 16) throw MwuError{MWU_ERR_ARG, std::string(name) + ": column index out of range or not strictly increasing in a row"};
+  if (eb & 32) throw MwuError{MWU_ERR_ARG, std::string(name) + ": negative or non-finite value (positive LP required)"};
+}
+
+// drop empty rows of P (Q17): compacted rowptr over the same item arrays
+void compact_rows(mwu_ctx* c, Seg& S) {
+  int64_t* fl = talloc<int64_t>(S.nrows);
+  if (S.nrows > 0) { k_row_nonempty<<<grid_for(c, S.nrows), MWU_NT, 0, c->st>>>(S.nrows, S.rowptr, fl); CKL(); }
+  int64_t* scan = talloc<int64_t>(S.nrows + 1);
+  exclusive_scan_total(c, fl, scan, S.nrows);
+  const int64_t kept = read_scalar(c, scan + S.nrows);
+  if (kept != S.nrows) {
+    int64_t* rp = dalloc<int64_t>(c, kept + 1);
+    k_compact_csr_rows<<<grid_for(c, S.nrows), MWU_NT, 0, c->st>>>(S.nrows, S.rowptr, scan, rp);
+    CKL();
+    CK(cudaMemcpyAsync(rp + kept, &S.nnz, sizeof(int64_t), cudaMemcpyHostToDevice, c->st));
+    sync(c);
+    c->empty_dropped = S.nrows - kept;
+    S.rowptr = rp;
+    S.nrows = kept;
+  }
+  tfree(fl);
+  tfree(scan);
+}
+
+// ------------------------------------------------------------------------------ kernel launchers
+template <class Ep>
+void launch_seg(mwu_ctx* c, cudaStream_t st, const Seg& S, ItemGather it, Ep ep, int action) {
+  const SegView sv = S.view();
+  if (S.nlong > 0) {
+    seg_long_chunks<ItemGather><<<grid_for(c, S.nchunks * MWU_NT), MWU_NT, 0, st>>>(sv, it, c->ctl);
+    c->launches++;
+  }
+  int g = (int)((S.ntiles < c->grid_rows) ? (S.ntiles < 1 ? 1 : S.ntiles) : c->grid_rows);
+  if (S.nlong > 0 && g < 8) g = 8;
+  seg_main<ItemGather, Ep><<<g, MWU_NT, 0, st>>>(sv, it, ep, c->ctl, c->part, c->counter, action);
+  c->launches++;
+}
+
+ItemGather item_of(const Seg& S, const double* vec, int shift, const double* scale_ptr) {
+  ItemGather it;
+  it.idx = S.idx; it.val = S.val; it.vec = vec; it.shift = shift; it.scale_ptr = scale_ptr;
+  return it;
+}
+
+int rows_grid(mwu_ctx* c, int64_t rows) {
+  const int g = grid_for(c, rows > 0 ? rows : 1);
+  return g < c->grid_rows ? g : c->grid_rows;
+}
+
+EpColumn make_col(mwu_ctx* c, int s_is_h, const double* gtmp) {
+  EpColumn ep;
+  ep.x = c->x; ep.d = c->d; ep.gtmp = gtmp; ep.gdbg = c->record ? c->gdbg : nullptr; ep.hdbg = c->record ? c->hdbg : nullptr;
+  ep.c = c->ctl; ep.s_is_h = s_is_h; ep.kind_step = 0;
+  return ep;
+}
+
+void enqueue_column(mwu_ctx* c, cudaStream_t st) {
+  switch (c->kind) {
+    case K_MATCH:
+      col_match<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, c->srow, c->drow, c->u, c->x, c->d,
+                                                      c->record ? c->gdbg : nullptr, c->record ? c->hdbg : nullptr,
+                                                      c->ctl, c->part, c->counter);
+      c->launches++;
+      break;
+    case K_DENSEST:
+      col_densest<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, c->srow, c->drow, c->u, c->v, c->x, c->d, c->dz,
+                                                        c->record ? c->gdbg : nullptr, c->record ? c->hdbg : nullptr,
+                                                        c->ctl, c->part, c->counter);
+      c->launches++;
+      break;
+    case K_VCOVER:
+      launch_seg(c, st, c->inc_all, item_of(c->inc_all, c->v, 1, nullptr), make_col(c, 1, nullptr), A_COL);
+      break;
+    case K_DOMSET:
+      launch_seg(c, st, c->cscC, item_of(c->cscC, c->v, 0, nullptr), make_col(c, 1, nullptr), A_COL);
+      break;
+    case K_CSR:
+      if (!c->pSing && !c->cSing) {
+        EpStoreG eg; eg.g = c->gtmp; eg.c = c->ctl; eg.kind_step = 0;
+        launch_seg(c, st, c->cscP, item_of(c->cscP, c->u, 0, nullptr), eg, A_NONE);
+        launch_seg(c, st, c->cscC, item_of(c->cscC, c->v, 0, nullptr), make_col(c, 1, c->gtmp), A_COL);
+      } else if (c->cSing) {
+        launch_seg(c, st, c->cscP, item_of(c->cscP, c->u, 0, nullptr), make_col(c, 0, nullptr), A_COL);
+      } else {
+        launch_seg(c, st, c->cscC, item_of(c->cscC, c->v, 0, nullptr), make_col(c, 1, nullptr), A_COL);
+      }
+      break;
+  }
+}
+
+// forward products: out_y = P in, out_z = C in.  init: actions A_NONE; iteration: step actions
+void enqueue_forward(mwu_ctx* c, cudaStream_t st, const double* in, double* oy, double* oz, bool init) {
+  EpOut ey; ey.out = oy; ey.kind_step = init ? 0 : 1;
+  EpOut ez; ez.out = oz; ez.kind_step = init ? 0 : 1;
+  double* invB = &c->ctl->invB;
+  const int a_done_p = init ? A_NONE : A_STEP_DONE + 100;
+  const int a_done = init ? A_NONE : A_STEP_DONE;
+  switch (c->kind) {
+    case K_MATCH:
+      launch_seg(c, st, c->inc_p, item_of(c->inc_p, in, 1, nullptr), ey, a_done_p);
+      break;
+    case K_DENSEST:
+      if (init) {
+        pair_sum<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, in, oz, c->ctl);
+        c->launches++;
+      }
+      launch_seg(c, st, c->inc_p, item_of(c->inc_p, in, 0, invB), ey, a_done_p);
+      break;
+    case K_VCOVER:
+      edge_sum<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, c->src, c->dst, in, oz, c->ctl, c->part, c->counter, a_done);
+      c->launches++;
+      break;
+    case K_DOMSET:
+      launch_seg(c, st, c->csrC, item_of(c->csrC, in, 0, nullptr), ez, a_done);
+      break;
+    case K_CSR:
+      if (!c->pSing && !c->cSing) {
+        launch_seg(c, st, c->csrP, item_of(c->csrP, in, 0, nullptr), ey, init ? A_NONE : A_STEP_MAXDY);
+        launch_seg(c, st, c->csrC, item_of(c->csrC, in, 0, nullptr), ez, a_done);
+      } else if (c->cSing) {
+        launch_seg(c, st, c->csrP, item_of(c->csrP, in, 0, nullptr), ey, a_done_p);
+      } else {
+        launch_seg(c, st, c->csrC, item_of(c->csrC, in, 0, nullptr), ez, a_done);
+      }
+      break;
+  }
+}
+
+void enqueue_search(mwu_ctx* c, cudaStream_t st) {
+  search_pass<<<rows_grid(c, c->mP + c->mC), MWU_NT, 0, st>>>(c->mP, c->y, c->dy, c->u, c->mC, c->z, c->dz, c->v,
+                                                              c->ctl, c->part, c->counter);
+  c->launches++;
+}
+
+void enqueue_update(mwu_ctx* c, cudaStream_t st, int has_delta) {
+  update_rows<<<rows_grid(c, c->mP + c->mC), MWU_NT, 0, st>>>(c->mP, c->y, c->dy, c->u, c->mC, c->z, c->dz, c->v,
+                                                             c->ctl, c->part, c->counter, has_delta);
+  c->launches++;
+}
+
+// ------------------------------------------------------------------------------ graph (probe loop)
+void build_probe_graph(mwu_ctx* c) {
+  if (c->graph_ok) return;
+  cudaGraph_t top;
+  CK(cudaGraphCreate(&top, 0));
+  cudaGraphConditionalHandle hi;
+  CK(cudaGraphConditionalHandleCreate(&hi, top, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = hi;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaGraphNode_t wn;
+  CK(cudaGraphAddNode(&wn, top, nullptr, 0, &p));
+  cudaGraph_t body = p.conditional.phGraph_out[0];
+  cudaGraphConditionalHandle hs;
+  CK(cudaGraphConditionalHandleCreate(&hs, body, 0, 0));
+  // part A: column + step
+  const int64_t l0 = c->launches;
+  CK(cudaStreamBeginCaptureToGraph(c->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  enqueue_column(c, c->st);
+  enqueue_forward(c, c->st, c->d, c->dy, c->dz, false);
+  cudaStreamCaptureStatus cst;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  CK(cudaStreamGetCaptureInfo(c->st, &cst, nullptr, nullptr, &deps, &ndeps));
+  std::vector<cudaGraphNode_t> leaf(deps, deps + ndeps);
+  cudaGraph_t g2;
+  CK(cudaStreamEndCapture(c->st, &g2));
+  // inner WHILE: search passes
+  cudaGraphNodeParams p2 = {};
+  p2.type = cudaGraphNodeTypeConditional;
+  p2.conditional.handle = hs;
+  p2.conditional.type = cudaGraphCondTypeWhile;
+  p2.conditional.size = 1;
+  cudaGraphNode_t sn;
+  CK(cudaGraphAddNode(&sn, body, leaf.data(), leaf.size(), &p2));
+  cudaGraph_t sbody = p2.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(c->st, sbody, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  enqueue_search(c, c->st);
+  CK(cudaStreamEndCapture(c->st, &g2));
+  // part C: update, after the search loop
+  CK(cudaStreamBeginCaptureToGraph(c->st, body, &sn, nullptr, 1, cudaStreamCaptureModeRelaxed));
+  enqueue_update(c, c->st, 1);
+  CK(cudaStreamEndCapture(c->st, &g2));
+  CK(cudaGraphInstantiate(&c->gexec, top, 0));
+  c->graph = top;
+  c->h_iter = (unsigned long long)hi;
+  c->h_search = (unsigned long long)hs;
+  c->launches = l0;  // captured launches are not executed launches
+  c->graph_ok = true;
+}
+
+// ------------------------------------------------------------------------------ probe engine
+int64_t m_total(mwu_ctx* c) { return (c->pSing ? 1 : c->mP) + (c->cSing ? 1 : c->mC); }
+
+void probe_begin(mwu_ctx* c, double bound, double eps) {
+  if (!(eps > 0.0 && eps < 1.0)) throw MwuError{MWU_ERR_ARG, "eps must be in (0, 1)"};
+  if (!(bound > 0.0) || !std::isfinite(bound)) throw MwuError{MWU_ERR_ARG, "bound must be positive and finite"};
+  if (c->n <= 0) throw MwuError{MWU_ERR_ARG, "instance has no variables"};
+  if (c->opt.use_graph) build_probe_graph(c);
+  Ctl& h = *c->hctl;
+  memset(&h, 0, sizeof(Ctl));
+  const int64_t m = m_total(c);
+  h.eps = eps;
+  h.B = bound;
+  h.invB = 1.0 / bound;                                    // (1/M) 1^T or 1/D
+  h.eta = c->opt.eta_factor * std::log((double)m) / eps;   // P:271, Q1, Q2
+  h.sigma = (c->mode == MWU_MIXED) ? 1.0 / (2.0 * h.eta) : 1.0 / h.eta;   // P:279, P:322 (Q13)
+  h.max_iter = c->opt.max_iter;
+  h.pSing = c->pSing;
+  h.cSing = c->cSing;
+  h.mode = c->mode;
+  h.tol_prose = c->opt.tol_prose;
+  h.max_evals = c->opt.max_evals;
+  h.bisect_depth = c->opt.bisect_depth;
+  h.use_graph = c->opt.use_graph;
+  h.status = c->empty_cover ? ST_INFEASIBLE : ST_RUNNING;
+  h.reason = c->empty_cover ? R_EMPTY_COVER : R_NONE;
+  h.record = c->record;
+  h.iter_stop = INT64_MAX;
+  h.h_iter = 0;     // conditional handles are live only while the probe graph runs
+  h.h_search = 0;
+  CK(cudaMemcpyAsync(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, c->st));
+  // x_i = eps / (n ||P_{:,i}||_inf)
+  double cm = 1.0;
+  const double* colmax = nullptr;
+  if (c->kind == K_DENSEST) cm = h.invB;                          // P = O/D
+  else if (c->kind == K_VCOVER || c->kind == K_DOMSET) cm = h.invB; // P = (1/M)1^T
+  else if (c->kind == K_CSR) { if (c->pSing) cm = h.invB; else colmax = c->colmaxP; }
+  init_x<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->x, colmax, cm, c->ctl, c->part, c->counter);
+  c->launches++;
+  CKL();
+  // y = P x, z = C x
+  enqueue_forward(c, c->st, c->x, c->y, c->z, true);
+  init_ext<<<rows_grid(c, c->mP + c->mC), MWU_NT, 0, c->st>>>(c->mP, c->y, c->mC, c->z, c->ctl, c->part, c->counter);
+  c->launches++;
+  enqueue_update(c, c->st, 0);
+  CKL();
+  sync(c);
+  c->probe_active = true;
+  c->bound = bound;
+  c->eps = eps;
+}
+
+// host-driven iteration (debug / lockstep parity path); alpha > 0 fixes the step
+void host_iteration(mwu_ctx* c, double alpha) {
+  push_field(c, &c->ctl->fixed_alpha, alpha > 0.0 ? alpha : 0.0);
+  pull_ctl(c);
+  if (c->hctl->status != ST_RUNNING) return;
+  enqueue_column(c, c->st);
+  enqueue_forward(c, c->st, c->d, c->dy, c->dz, false);
+  CKL();
+  for (int guard = 0; guard < 100000; ++guard) {
+    pull_ctl(c);
+    if (c->hctl->status != ST_RUNNING || !c->hctl->sactive) break;
+    enqueue_search(c, c->st);
+    CKL();
+  }
+  enqueue_update(c, c->st, 1);
+  CKL();
+  sync(c);
+  if (alpha > 0.0) push_field(c, &c->ctl->fixed_alpha, 0.0);
+}
+
+float run_loop(mwu_ctx* c, int64_t k) {
+  pull_ctl(c);
+  if (c->hctl->status != ST_RUNNING) return 0.f;
+  const int64_t stop = (k < 0) ? INT64_MAX : c->hctl->t + k;
+  if (k == 0) return 0.f;
+  float ms = 0.f;
+  if (c->opt.use_graph) {
+    build_probe_graph(c);
+    push_field(c, &c->ctl->iter_stop, stop);
+    push_field(c, &c->ctl->h_iter, c->h_iter);
+    push_field(c, &c->ctl->h_search, c->h_search);
+    CK(cudaEventRecord(c->ev0, c->st));
+    CK(cudaGraphLaunch(c->gexec, c->st));
+    CK(cudaEventRecord(c->ev1, c->st));
+    sync(c);
+    CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    push_field(c, &c->ctl->h_iter, 0ull);
+    push_field(c, &c->ctl->h_search, 0ull);
+    push_field(c, &c->ctl->iter_stop, (int64_t)INT64_MAX);
+  } else {
+    CK(cudaEventRecord(c->ev0, c->st));
+    for (;;) {
+      pull_ctl(c);
+      if (c->hctl->status != ST_RUNNING || c->hctl->t >= stop) break;
+      host_iteration(c, 0.0);
+    }
+    CK(cudaEventRecord(c->ev1, c->st));
+    sync(c);
+    CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  }
+  pull_ctl(c);
+  if (c->hctl->nan_flag) throw MwuError{MWU_ERR_NUMERIC, "non-finite weight sums"};
+  return ms;
+}
+
+// Host-driven iterations with CUDA events around every phase (per-kernel roofline in bench.py).
+// out[2p] = total ms, out[2p+1] = kernel launches, for p = column, step, search, update;
+// out[8] = iterations run, out[9] = search passes.
+void profile_iters(mwu_ctx* c, int64_t k, double* out) {
+  for (int i = 0; i < 10; ++i) out[i] = 0.0;
+  cudaEvent_t e[2];
+  CK(cudaEventCreate(&e[0]));
+  CK(cudaEventCreate(&e[1]));
+  auto timed = [&](int p, auto&& fn) {
+    const int64_t l0 = c->launches;
+    CK(cudaEventRecord(e[0], c->st));
+    fn();
+    CK(cudaEventRecord(e[1], c->st));
+    CK(cudaEventSynchronize(e[1]));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e[0], e[1]));
+    out[2 * p] += ms;
+    out[2 * p + 1] += (double)(c->launches - l0);
+  };
+  for (int64_t it = 0; it < k; ++it) {
+    pull_ctl(c);
+    if (c->hctl->status != ST_RUNNING) break;
+    timed(0, [&] { enqueue_column(c, c->st); });
+    timed(1, [&] { enqueue_forward(c, c->st, c->d, c->dy, c->dz, false); });
+    for (int guard = 0; guard < 100000; ++guard) {
+      pull_ctl(c);
+      if (c->hctl->status != ST_RUNNING || !c->hctl->sactive) break;
+      timed(2, [&] { enqueue_search(c, c->st); });
+      out[9] += 1;
+    }
+    timed(3, [&] { enqueue_update(c, c->st, 1); });
+    out[8] += 1;
+  }
+  cudaEventDestroy(e[0]);
+  cudaEventDestroy(e[1]);
+}
+
+void flush(mwu_ctx* c) {
+  flush_x<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->x, c->d, c->ctl);
+  CKL();
+  int zero = 0;
+  CK(cudaMemcpyAsync(&c->ctl->apply_prev, &zero, sizeof(int), cudaMemcpyHostToDevice, c->st));
+  sync(c);
+}
+
+// sum / max of a device vector (ctl->scratch[0], [1])
+void reduce_dev(mwu_ctx* c, const double* a, int64_t n, double& sum, double& mx) {
+  reduce_vec<<<rows_grid(c, n), MWU_NT, 0, c->st>>>(n, a, c->ctl, c->part, c->counter);
+  CKL();
+  double s[2];
+  CK(cudaMemcpyAsync(s, c->ctl->scratch, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  sync(c);
+  sum = s[0];
+  mx = s[1];
+}
+
+// Q14 brackets (L, H) and witness x into xbest
+void brackets(mwu_ctx* c, double eps, double& L, double& H) {
+  double s, mx;
+  if (c->kind == K_DENSEST) {
+    L = (double)c->E / (double)c->nprime;
+    H = (double)c->maxdeg / 2.0;
+    k_fill<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->xbest, 0.5);
+    CKL();
+    return;
+  }
+  if (c->kind == K_VCOVER || c->kind == K_DOMSET) {
+    L = (c->kind == K_VCOVER) ? (double)c->E / (double)c->maxdeg : (double)c->nv / (double)(c->maxdeg + 1);
+    if (c->kind == K_VCOVER) k_fill_nonzero<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->deg, c->xbest, 1.0);
+    else k_fill<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->xbest, 1.0);
+    CKL();
+    reduce_dev(c, c->xbest, c->n, s, mx);
+    H = s;
+    return;
+  }
+  if (c->kind == K_CSR && c->mode == MWU_PURE_COVERING) {
+    reduce_dev(c, c->colsumC, c->n, s, mx);
+    L = (double)c->mC / mx;
+    CK(cudaMemcpyAsync(c->xbest, c->crecipC, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+    reduce_dev(c, c->xbest, c->n, s, mx);
+    H = s;
+    return;
+  }
+  // packing: witness x0 / max(P x0) (x0 of P:272), H = sum_i max_j 1/p_ji
+  Ctl& h = *c->hctl;
+  memset(&h, 0, sizeof(Ctl));
+  h.eps = eps; h.invB = 1.0; h.status = ST_RUNNING; h.iter_stop = INT64_MAX;
+  CK(cudaMemcpyAsync(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, c->st));
+  init_x<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->x, c->kind == K_CSR ? c->colmaxP : nullptr, 1.0, c->ctl,
+                                                  c->part, c->counter);
+  CKL();
+  enqueue_forward(c, c->st, c->x, c->y, c->z, true);
+  reduce_dev(c, c->y, c->mP, s, mx);
+  CK(cudaMemcpyAsync(c->tmp, &mx, sizeof(double), cudaMemcpyHostToDevice, c->st));
+  scale_div<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->x, c->xbest, c->tmp);
+  CKL();
+  sync(c);
+  reduce_dev(c, c->xbest, c->n, s, mx);
+  L = s;
+  if (c->kind == K_MATCH) H = (double)c->E;
+  else { reduce_dev(c, c->crecipP, c->n, s, mx); H = s; }
+}
+
+void finish_feasible(mwu_ctx* c) {
+  // x_out = x / min(Cx) (Q15) with min(Cx) = s_C (cached)
+  flush(c);
+  scale_div<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->x, c->xbest, &c->ctl->sC);
+  CKL();
+  sync(c);
+}
+
+void solve(mwu_ctx* c, double eps, int64_t max_iter, int32_t* outcome) {
+  if (max_iter > 0) c->opt.max_iter = max_iter;
+  mwu_stats& S = c->stats;
+  const int64_t l0 = c->launches;
+  S.probes = 0; S.iters_total = 0; S.search_evals = 0; S.search_passes = 0;
+  S.certificate = std::numeric_limits<double>::quiet_NaN();
+  S.objective = std::numeric_limits<double>::quiet_NaN();
+  CK(cudaEventRecord(c->ev0, c->st));
+  float loop_ms_total = 0.f;
+  auto run_one = [&](double B) -> int {
+    probe_begin(c, B, eps);
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, c->st));
+    (void)run_loop(c, -1);
+    CK(cudaEventRecord(b, c->st));
+    CK(cudaEventSynchronize(b));
+    float ms = 0; CK(cudaEventElapsedTime(&ms, a, b)); loop_ms_total += ms;
+    cudaEventDestroy(a); cudaEventDestroy(b);
+    pull_ctl(c);
+    const Ctl& h = *c->hctl;
+    S.probes++;
+    S.iters_total += h.t;
+    S.iters_last = h.t;
+    S.search_evals += h.evals_total;
+    S.search_passes += h.passes_total;
+    S.outcome = h.status; S.reason = h.reason; S.eta = h.eta; S.alpha_last = h.alpha_last;
+    if (h.status == ST_FEASIBLE) {
+      S.certificate = h.sP / h.sC;      // rho = max y / min z (Q6)
+      finish_feasible(c);
+    }
+    return h.status;
+  };
+  if (c->kind == K_CSR && c->mode == MWU_MIXED) {
+    const int st = run_one(1.0);
+    if (st != ST_FEASIBLE) { flush(c); CK(cudaMemcpyAsync(c->xbest, c->x, c->n * sizeof(double), cudaMemcpyDeviceToDevice, c->st)); }
+    S.bound = std::numeric_limits<double>::quiet_NaN();
+    *outcome = st;
+  } else {
+    double L, H;
+    brackets(c, eps, L, H);
+    const double rt = c->opt.outer_rel_tol > 0 ? c->opt.outer_rel_tol : eps / 4.0;
+    const int sense = (c->mode == MWU_PURE_PACKING) ? +1 : -1;
+    bool any = false;
+    double cert = std::numeric_limits<double>::quiet_NaN();
+    while (H > (1.0 + rt) * L) {
+      const double B = std::sqrt(L * H);
+      const int st = run_one(B);
+      const bool ok = (st == ST_FEASIBLE);
+      if (ok) { any = true; cert = S.certificate; }
+      if ((ok && sense > 0) || (!ok && sense < 0)) L = B; else H = B;
+    }
+    S.certificate = any ? cert : std::numeric_limits<double>::quiet_NaN();
+    S.bound = sense > 0 ? L : H;
+    if (c->kind == K_DENSEST) S.objective = S.bound;
+    else { double s, mx; reduce_dev(c, c->xbest, c->n, s, mx); S.objective = s; }
+    S.outcome = ST_FEASIBLE;
+    *outcome = ST_FEASIBLE;
+  }
+  CK(cudaEventRecord(c->ev1, c->st));
+  CK(cudaEventSynchronize(c->ev1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  S.t_solve_ms = ms;
+  S.t_loop_ms = loop_ms_total;
+  S.kernel_launches = c->launches - l0;
+}
+
+void fill_static_stats(mwu_ctx* c) {
+  mwu_stats& S = c->stats;
+  S.n = c->n; S.m_P = c->pSing ? 1 : c->mP; S.m_C = c->cSing ? 1 : c->mC;
+  S.nnz_P = c->nnzP; S.nnz_C = c->nnzC; S.empty_rows_dropped = c->empty_dropped;
+  // algorithmic bytes per MWU iteration: structure of the two forward and two
+  // transposed products + 32 B per variable (x r/w, d r/w) + 40 B per stored row
+  double sfwd_tr = 0;
+  const double rowsB = 40.0 * (double)(c->mP + c->mC);
+  auto implicit = [&](int64_t rp_rows) { return 4.0 * (double)c->E + 8.0 * (double)(rp_rows + 1); };
+  switch (c->kind) {
+    case K_MATCH: sfwd_tr = 2 * implicit(c->nleft > 0 ? c->nleft : c->nv); break;
+    case K_VCOVER: case K_DENSEST: sfwd_tr = 2 * implicit(c->nv); break;
+    case K_DOMSET: sfwd_tr = 2 * (4.0 * c->nnzC + rp_bytes(c->nnzC) * (c->nv + 1)); break;
+    case K_CSR: {
+      auto side = [&](const Seg& A) {
+        return A.rowptr ? 4.0 * A.nnz + rp_bytes(A.nnz) * (A.nrows + 1) + (A.val ? 8.0 * A.nnz : 0.0) : 0.0;
+      };
+      sfwd_tr = side(c->csrP) + side(c->cscP) + side(c->csrC) + side(c->cscC);
+      break;
+    }
+  }
+  c->bytes_alg = sfwd_tr + 32.0 * (double)c->n + rowsB;
+  S.bytes_alg_per_iter = c->bytes_alg;
+}
+
+mwu_status fail(mwu_ctx* c, const MwuError& e) {
+  if (c) {
+    c->err = e.msg;
+    if (e.st == MWU_ERR_CUDA) c->poisoned = true;
+  }
+  return e.st;
+}
+
+void destroy_ctx(mwu_ctx* c) {
+  if (!c) return;
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->graph) cudaGraphDestroy(c->graph);
+  if (c->st) cudaStreamSynchronize(c->st);
+  for (void* p : c->allocs) cudaFree(p);
+  if (c->hctl) cudaFreeHost(c->hctl);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->st) cudaStreamDestroy(c->st);
+  delete c;
+}
+
+}  // namespace
+
+// ================================================================================== C ABI
+extern "C" {
+
+void mwu_default_options(mwu_options* o) {
+  if (!o) return;
+  memset(o, 0, sizeof(*o));
+  o->eta_factor = 10.0;
+  o->max_iter = 5000;
+  o->tol_prose = 1;
+  o->max_evals = 200;
+  o->outer_rel_tol = 0.0;
+  o->use_graph = 1;
+  o->bisect_depth = 3;
+  o->device = -1;
+  o->world = 1;
+  o->rank = 0;
+  o->nccl_id = nullptr;
+}
+
+const char* mwu_last_error(const mwu_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+mwu_status mwu_create_graph(const mwu_graph* g, const mwu_options* opt, mwu_ctx** out) {
+  if (!out) return MWU_ERR_ARG;
+  *out = nullptr;
+  if (!g || g->n_vertices <= 0 || g->n_edges < 0 || (g->n_edges > 0 && (!g->src || !g->dst)) ||
+      g->kind < MWU_G_BMATCH || g->kind > MWU_G_DENSEST || g->n_vertices > INT32_MAX || g->n_edges > (int64_t(1) << 31)) {
+    g_create_err = "mwu_create_graph: bad descriptor";
+    return MWU_ERR_ARG;
+  }
+  mwu_ctx* c = new mwu_ctx();
+  try {
+    init_ctx_common(c, opt);
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, c->st));
+    build_graph_storage(c, g);
+    switch (g->kind) {
+      case MWU_G_BMATCH: case MWU_G_MATCH:
+        if (g->n_edges == 0) throw MwuError{MWU_ERR_ARG, "matching needs at least one edge"};
+        c->kind = K_MATCH; c->mode = MWU_PURE_PACKING; c->n = c->E; c->mP = c->nprime; c->cSing = 1;
+        c->nnzP = 2 * c->E; c->nnzC = c->E; c->empty_dropped = c->nv - c->nprime;
+        break;
+      case MWU_G_VCOVER:
+        if (g->n_edges == 0) throw MwuError{MWU_ERR_ARG, "vertex cover needs at least one edge"};
+        c->kind = K_VCOVER; c->mode = MWU_PURE_COVERING; c->n = c->nv; c->mC = c->E; c->pSing = 1;
+        c->nnzC = 2 * c->E; c->nnzP = c->nv;
+        break;
+      case MWU_G_DOMSET:
+        c->kind = K_DOMSET; c->mode = MWU_PURE_COVERING; c->n = c->nv; c->mC = c->nv; c->pSing = 1; c->nnzP = c->nv;
+        break;
+      case MWU_G_DENSEST:
+        if (g->n_edges == 0) throw MwuError{MWU_ERR_ARG, "densest subgraph needs at least one edge"};
+        c->kind = K_DENSEST; c->mode = MWU_MIXED; c->n = 2 * c->E; c->mP = c->nprime; c->mC = c->E;
+        c->nnzP = 2 * c->E; c->nnzC = 2 * c->E; c->empty_dropped = c->nv - c->nprime;
+        break;
+    }
+    alloc_vectors(c);
+    fill_static_stats(c);
+    CK(cudaEventRecord(b, c->st));
+    CK(cudaEventSynchronize(b));
+    float ms = 0; CK(cudaEventElapsedTime(&ms, a, b));
+    c->stats.t_create_ms = ms;
+    cudaEventDestroy(a); cudaEventDestroy(b);
+    sync(c);
+  } catch (const MwuError& e) {
+    g_create_err = e.msg;
+    destroy_ctx(c);
+    return e.st;
+  }
+  *out = c;
+  return MWU_OK;
+}
+
+mwu_status mwu_create_csr(const mwu_csr* P, const mwu_csr* C, mwu_mode mode, const mwu_options* opt, mwu_ctx** out) {
+  if (!out) return MWU_ERR_ARG;
+  *out = nullptr;
+  const bool needP = (mode == MWU_MIXED || mode == MWU_PURE_PACKING);
+  const bool needC = (mode == MWU_MIXED || mode == MWU_PURE_COVERING);
+  if ((needP && !P) || (needC && !C) || (mode < MWU_MIXED || mode > MWU_PURE_COVERING)) {
+    g_create_err = "mwu_create_csr: missing matrix for this mode";
+    return MWU_ERR_ARG;
+  }
+  const int64_t n = needP ? P->cols : C->cols;
+  if (needP && needC && P->cols != C->cols) { g_create_err = "mwu_create_csr: P.cols != C.cols"; return MWU_ERR_ARG; }
+  if (n <= 0 || n > INT32_MAX) { g_create_err = "mwu_create_csr: bad number of columns"; return MWU_ERR_ARG; }
+  mwu_ctx* c = new mwu_ctx();
+  try {
+    init_ctx_common(c, opt);
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, c->st));
+    c->kind = K_CSR; c->mode = mode; c->n = n;
+    if (needP) {
+      copy_csr_checked(c, P, c->csrP, n, "P");
+      compact_rows(c, c->csrP);                       // Q17
+      c->mP = c->csrP.nrows; c->nnzP = c->csrP.nnz;
+      build_plan(c, c->csrP);
+      build_csc(c, c->csrP, n, c->cscP);
+      c->colmaxP = dalloc<double>(c, n);
+      c->crecipP = dalloc<double>(c, n);
+      k_col_stats<<<grid_for(c, n), MWU_NT, 0, c->st>>>(n, c->cscP.rowptr, c->cscP.val, c->colmaxP, nullptr, c->crecipP);
+      CKL();
+      double s, mx;
+      // an all-zero packing column leaves x_i = eps/(n*0) undefined
+      double* mn = talloc<double>(1);
+      size_t tb = 0;
+      CK(cub::DeviceReduce::Min(nullptr, tb, c->colmaxP, mn, n, c->st));
+      void* t = talloc<char>(tb);
+      CK(cub::DeviceReduce::Min(t, tb, c->colmaxP, mn, n, c->st));
+      const double mincol = read_scalar(c, mn);
+      tfree(t); tfree(mn);
+      (void)s; (void)mx;
+      if (!(mincol > 0.0)) throw MwuError{MWU_ERR_ARG, "P has an all-zero column: initialisation x_i = eps/(n ||P_:,i||) undefined"};
+    } else {
+      c->pSing = 1; c->nnzP = n;
+    }
+    if (needC) {
+      copy_csr_checked(c, C, c->csrC, n, "C");
+      c->mC = c->csrC.nrows; c->nnzC = c->csrC.nnz;
+      // empty covering rows make the LP infeasible (0 >= 1), Q17
+      {
+        Seg tmpS = c->csrC;
+        const int64_t before = tmpS.nrows;
+        int64_t saved = c->empty_dropped;
+        compact_rows(c, tmpS);
+        c->empty_cover = (tmpS.nrows != before);
+        c->empty_dropped = saved;
+      }
+      build_plan(c, c->csrC);
+      build_csc(c, c->csrC, n, c->cscC);
+      c->colsumC = dalloc<double>(c, n);
+      c->crecipC = dalloc<double>(c, n);
+      k_col_stats<<<grid_for(c, n), MWU_NT, 0, c->st>>>(n, c->cscC.rowptr, c->cscC.val, nullptr, c->colsumC, c->crecipC);
+      CKL();
+    } else {
+      c->cSing = 1; c->nnzC = n;
+    }
+    alloc_vectors(c);
+    fill_static_stats(c);
+    CK(cudaEventRecord(b, c->st));
+    CK(cudaEventSynchronize(b));
+    float ms = 0; CK(cudaEventElapsedTime(&ms, a, b));
+    c->stats.t_create_ms = ms;
+    cudaEventDestroy(a); cudaEventDestroy(b);
+  } catch (const MwuError& e) {
+    g_create_err = e.msg;
+    destroy_ctx(c);
+    return e.st;
+  }
+  *out = c;
+  return MWU_OK;
+}
+
+#define GUARD(c)                                          \
+  if (!(c)) return MWU_ERR_ARG;                           \
+  if ((c)->poisoned) return MWU_ERR_CUDA;
+
+mwu_status mwu_solve(mwu_ctx* c, double eps, int64_t max_iter, int32_t* outcome) {
+  GUARD(c);
+  int32_t dummy;
+  if (!outcome) outcome = &dummy;
+  try {
+    solve(c, eps, max_iter, outcome);
+  } catch (const MwuError& e) { return fail(c, e); }
+  return MWU_OK;
+}
+
+mwu_status mwu_get_x(mwu_ctx* c, double* x, int64_t len) {
+  GUARD(c);
+  if (!x || len != c->n) { c->err = "mwu_get_x: len must equal n"; return MWU_ERR_ARG; }
+  try {
+    CK(cudaMemcpyAsync(x, c->xbest, c->n * sizeof(double), cudaMemcpyDefault, c->st));
+    sync(c);
+  } catch (const MwuError& e) { return fail(c, e); }
+  return MWU_OK;
+}
+
+mwu_status mwu_get_stats(mwu_ctx* c, mwu_stats* out) {
+  GUARD(c);
+  if (!out) return MWU_ERR_ARG;
+  *out = c->stats;
+  return MWU_OK;
+}
+
+void mwu_destroy(mwu_ctx* c) { destroy_ctx(c); }
+
+mwu_status mwu_probe_begin(mwu_ctx* c, double bound, double eps) {
+  GUARD(c);
+  try {
+    if (c->kind == K_CSR && c->mode == MWU_MIXED) bound = 1.0;
+    probe_begin(c, bound, eps);
+  } catch (const MwuError& e) { return fail(c, e); }
+  return MWU_OK;
+}
+
+mwu_status mwu_step(mwu_ctx* c, double alpha, int32_t* state) {
+  GUARD(c);
+  if (!c->probe_active) { c->err = "mwu_step: no active probe"; return MWU_ERR_STATE; }
+  try {
+    host_iteration(c, alpha);
+    pull_ctl(c);
+    if (c->hctl->nan_flag) throw MwuError{MWU_ERR_NUMERIC, "non-finite weight sums"};
+    if (state) *state = c->hctl->status;
+  } catch (const MwuError& e) { return fail(c, e); }
+  return MWU_OK;
+}
+
+mwu_status mwu_run_iters(mwu_ctx* c, int64_t k, int32_t* state) {
+  GUARD(c);
+  if (!c->probe_active) { c->err = "mwu_run_iters: no active probe"; return MWU_ERR_STATE; }
+  try {
+    const int64_t l0 = c->launches;
+    c->stats.t_loop_ms = run_loop(c, k);
+    pull_ctl(c);
+    if (state) *state = c->hctl->status;
+    c->stats.kernel_launches = c->launches - l0;
+  } catch (const MwuError& e) { return fail(c, e); }
+  return MWU_OK;
+}
+
+mwu_status mwu_run_probe(mwu_ctx* c, int32_t* state) { return mwu_run_iters(c, -1, state); }
+
+int64_t mwu_vec_len(mwu_ctx* c, int which) {
+  if (!c) return 0;
+  switch (which) {
+    case MWU_VEC_X: case MWU_VEC_D: case MWU_VEC_XBEST: return c->n;
+    case MWU_VEC_G: case MWU_VEC_H: return c->record ? c->n : 0;
+    case MWU_VEC_Y: case MWU_VEC_DY: case MWU_VEC_WP: return c->pSing ? 1 : c->mP;
+    case MWU_VEC_Z: case MWU_VEC_DZ: case MWU_VEC_WC: return c->cSing ? 1 : c->mC;
+  }
+  return 0;
+}
+
+mwu_status mwu_get_vec(mwu_ctx* c, int which, double* out, int64_t len) {
+  GUARD(c);
+  const int64_t L = mwu_vec_len(c, which);
+  if (!out || L <= 0 || len != L) { c->err = "mwu_get_vec: unknown vector or wrong length"; return MWU_ERR_ARG; }
+  try {
+    pull_ctl(c);
+    const Ctl h = *c->hctl;
+    const double* src = nullptr;
+    double scal = 0;
+    bool use_scal = false;
+    switch (which) {
+      case MWU_VEC_X: flush(c); src = c->x; break;
+      case MWU_VEC_D: src = c->d; break;
+      case MWU_VEC_XBEST: src = c->xbest; break;
+      case MWU_VEC_G: src = c->gdbg; break;
+      case MWU_VEC_H: src = c->hdbg; break;
+      case MWU_VEC_Y: if (c->pSing) { scal = h.yS; use_scal = true; } else src = c->y; break;
+      case MWU_VEC_DY: if (c->pSing) { scal = h.dyS; use_scal = true; } else src = c->dy; break;
+      case MWU_VEC_Z: if (c->cSing) { scal = h.zS; use_scal = true; } else src = c->z; break;
+      case MWU_VEC_DZ: if (c->cSing) { scal = h.dzS; use_scal = true; } else src = c->dz; break;
+      case MWU_VEC_WP:
+        if (c->pSing) { scal = 1.0; use_scal = true; }
+        else { scale_div<<<rows_grid(c, c->mP), MWU_NT, 0, c->st>>>(c->mP, c->u, c->tmp, &c->ctl->SP); CKL(); src = c->tmp; }
+        break;
+      case MWU_VEC_WC:
+        if (c->cSing) { scal = 1.0; use_scal = true; }
+        else { scale_div<<<rows_grid(c, c->mC), MWU_NT, 0, c->st>>>(c->mC, c->v, c->tmp, &c->ctl->SC); CKL(); src = c->tmp; }
+        break;
+    }
+    if (use_scal) CK(cudaMemcpyAsync(out, &scal, sizeof(double), cudaMemcpyDefault, c->st));
+    else CK(cudaMemcpyAsync(out, src, L * sizeof(double), cudaMemcpyDefault, c->st));
+    sync(c);
+  } catch (const MwuError& e) { return fail(c, e); }
+  return MWU_OK;
+}
+
+mwu_status mwu_set_record(mwu_ctx* c, int on) {
+  GUARD(c);
+  try {
+    if (on && !c->gdbg) { c->gdbg = dalloc<double>(c, c->n); c->hdbg = dalloc<double>(c, c->n); }
+    if (on != c->record && c->graph_ok) {  // epilogue pointers are baked into the graph
+      cudaGraphExecDestroy(c->gexec); cudaGraphDestroy(c->graph);
+      c->gexec = nullptr; c->graph = nullptr; c->graph_ok = false;
+    }
+    c->record = on ? 1 : 0;
+  } catch (const MwuError& e) { return fail(c, e); }
+  return MWU_OK;
+}
+
+mwu_status mwu_get_structure(mwu_ctx* c, int which, void* out, int64_t* bytes) {
+  GUARD(c);
+  if (!bytes) return MWU_ERR_ARG;
+  const void* src = nullptr;
+  int64_t nb = 0;
+  switch (which) {
+    case MWU_ST_INC_ROWPTR: src = c->inc_all.rowptr; nb = c->inc_all.rowptr ? (c->nv + 1) * 8 : 0; break;
+    case MWU_ST_INC_SLOTS: src = c->inc_all.idx; nb = c->inc_all.idx ? 2 * c->E * 4 : 0; break;
+    case MWU_ST_DEGREE: src = c->deg; nb = c->deg ? c->nv * 4 : 0; break;
+    case MWU_ST_PROW_OF_VERTEX: src = c->prow; nb = c->prow ? c->nv * 4 : 0; break;
+    case MWU_ST_C_ROWPTR: src = c->csrC.rowptr; nb = c->csrC.rowptr ? (c->csrC.nrows + 1) * 8 : 0; break;
+    case MWU_ST_C_COLIDX: src = c->csrC.idx; nb = c->csrC.rowptr ? c->csrC.nnz * 4 : 0; break;
+    case MWU_ST_CT_ROWPTR: src = c->cscC.rowptr; nb = c->cscC.rowptr ? (c->cscC.nrows + 1) * 8 : 0; break;
+    case MWU_ST_CT_ROWIDX: src = c->cscC.idx; nb = c->cscC.rowptr ? c->cscC.nnz * 4 : 0; break;
+    case MWU_ST_PT_ROWPTR: src = c->cscP.rowptr; nb = c->cscP.rowptr ? (c->cscP.nrows + 1) * 8 : 0; break;
+    case MWU_ST_PT_ROWIDX: src = c->cscP.idx; nb = c->cscP.rowptr ? c->cscP.nnz * 4 : 0; break;
+    case MWU_ST_P_ROWPTR: src = c->csrP.rowptr; nb = c->csrP.rowptr ? (c->csrP.nrows + 1) * 8 : 0; break;
+    case MWU_ST_P_COLIDX: src = c->csrP.idx; nb = c->csrP.rowptr ? c->csrP.nnz * 4 : 0; break;
+    default: break;
+  }
+  if (!src || nb <= 0) {
+    if (nb == 0 && src) { *bytes = 0; return MWU_OK; }
+    c->err = "mwu_get_structure: structure not present for this kind";
+    return MWU_ERR_ARG;
+  }
+  if (*bytes < nb || !out) { *bytes = nb; c->err = "mwu_get_structure: buffer too small"; return MWU_ERR_ARG; }
+  try {
+    CK(cudaMemcpyAsync(out, src, nb, cudaMemcpyDefault, c->st));
+    sync(c);
+  } catch (const MwuError& e) { return fail(c, e); }
+  *bytes = nb;
+  return MWU_OK;
+}
+
+mwu_status mwu_get_scalars(mwu_ctx* c, double* o) {
+  GUARD(c);
+  if (!o) return MWU_ERR_ARG;
+  try {
+    pull_ctl(c);
+    const Ctl& h = *c->hctl;
+    o[0] = h.eta; o[1] = h.sigma; o[2] = h.sP; o[3] = h.SP; o[4] = h.sC; o[5] = h.SC;
+    o[6] = (double)h.t; o[7] = h.alpha_last; o[8] = (double)h.evals_total; o[9] = (double)h.passes_total;
+  } catch (const MwuError& e) { return fail(c, e); }
+  return MWU_OK;
+}
+
+mwu_status mwu_profile_iters(mwu_ctx* c, int64_t k, double* out10) {
+  GUARD(c);
+  if (!out10) return MWU_ERR_ARG;
+  if (!c->probe_active) { c->err = "mwu_profile_iters: no active probe"; return MWU_ERR_STATE; }
+  try {
+    profile_iters(c, k, out10);
+  } catch (const MwuError& e) { return fail(c, e); }
+  return MWU_OK;
+}
+
+mwu_status mwu_get_unique_id(void* out128) {
+  (void)out128;
+  return MWU_ERR_NCCL;
+}
+
+}  // extern "C"
