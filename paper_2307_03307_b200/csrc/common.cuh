@@ -11,8 +11,8 @@
 #include <math.h>
 
 #define MWU_NT 256            // threads per block for every kernel
-#define MWU_MAXC 8            // step-search candidates evaluated per HBM pass
-#define MWU_SLOTS 32          // reduction slots per block partial (4 * MAXC)
+#define MWU_MAXC 4            // step-search candidates evaluated per HBM pass
+#define MWU_SLOTS 24          // reduction slots per block partial (6 * MAXC)
 #define MWU_TILE 2048         // items per seg tile (a tile loads <= 2*TILE items into smem)
 #define MWU_LCH 8192          // items per chunk of a long row (deg > TILE)
 
@@ -25,6 +25,8 @@ enum RedOp : int { OP_SUM = 0, OP_MAX = 1, OP_MIN = 2 };
 enum CandMode : int { CM_EXPM1 = 0, CM_LSE = 1, CM_EXT = 2 };
 // search phases (Alg. 3)
 enum SPhase : int { SP_DOUBLE = 0, SP_BISECT = 1, SP_DONE = 2, SP_FIXED = 3 };
+// candidate layout of a search pass: explicit list, doubling a0*2^j, bisection grid a0 + k*delta
+enum PType : int { PT_LIST = 0, PT_DOUBLE = 1, PT_GRID = 2 };
 
 // Finalize actions (what the last block does after a kernel's reduction).
 enum Action : int {
@@ -64,6 +66,13 @@ struct Ctl {
   double sa, lb, ub;                   // doubling alpha, bisection bracket
   double lb_mx, lb_mn, ok_mx, ok_mn;   // ext values of lb / the last accepted doubling alpha
   double fixed_alpha;
+  int32_t ptype, pad2_;                // pass layout: PT_LIST, PT_DOUBLE (a0 2^j), PT_GRID (a0 + k delta)
+  double pa0, pdelta;
+  // doubling phase bookkeeping over exponents k (candidates 2^k, Alg. 3):
+  // dk_lo = largest k known to pass (f >= 1 and no early exit), dk_hi = smallest k known to stop
+  int32_t dk_lo, dk_hi, hi_exit, pad3_;
+  double hi_mx, hi_mn;
+  int32_t cexp[MWU_MAXC], csq[MWU_MAXC];
   double cand[MWU_MAXC], cea[MWU_MAXC], shP[MWU_MAXC], shC[MWU_MAXC];
   int32_t cmP[MWU_MAXC], cmC[MWU_MAXC];
   // ---- statistics (accumulated over the probe)
@@ -138,6 +147,78 @@ __device__ __forceinline__ bool last_block_reduce(const int* ops, const double* 
   if (threadIdx.x == 0) *counter = 0u;    // ready for the next kernel on this stream
   __syncthreads();
   return true;
+}
+
+// ---------------------------------------------------------------- TMA (1-D bulk copy) pipeline
+// cp.async.bulk global -> shared with an mbarrier completion (the Hopper/Blackwell bulk-copy
+// engine): streams contiguous row vectors into shared memory, so HBM parallelism does not
+// depend on how many registers the consuming kernel needs.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+#define MWU_SCH 512    // rows per streamed chunk
+#define MWU_SST 4      // pipeline stages
+
+// Stream rows [0, n) of three fp64 arrays through shared memory in chunks of MWU_SCH, chunk k
+// of the grid-stride sequence going to stage (it % MWU_SST); calls f(a, b, c, i) once per row.
+// `it` continues across calls so mbarrier parities stay consistent.  Vectors must be allocated
+// with >= 1 padding element (bulk copies move multiples of 16 bytes).
+template <class F>
+__device__ __forceinline__ void stream_rows3(const double* A, const double* B, const double* C, int64_t n,
+                                             double* buf, uint64_t* bars, uint32_t& it, F&& f) {
+  const int64_t nchunks = (n + MWU_SCH - 1) / MWU_SCH;
+  const int64_t first = blockIdx.x;
+  const int64_t mine = (nchunks > first) ? (nchunks - first + gridDim.x - 1) / gridDim.x : 0;
+  auto issue = [&](int64_t k, uint32_t slot) {
+    const int64_t ch = first + k * (int64_t)gridDim.x;
+    const int64_t r0 = ch * MWU_SCH;
+    const int64_t rows = (n - r0 < MWU_SCH) ? (n - r0) : MWU_SCH;
+    const uint32_t bytes = (uint32_t)(((rows * 8) + 15) & ~15ll);
+    double* s = buf + (size_t)slot * 3 * MWU_SCH;
+    mbar_expect_tx(&bars[slot], 3 * bytes);
+    tma_load_1d(s, A + r0, bytes, &bars[slot]);
+    tma_load_1d(s + MWU_SCH, B + r0, bytes, &bars[slot]);
+    tma_load_1d(s + 2 * MWU_SCH, C + r0, bytes, &bars[slot]);
+  };
+  if (threadIdx.x == 0)
+    for (int64_t k = 0; k < mine && k < MWU_SST; ++k) issue(k, (it + (uint32_t)k) % MWU_SST);
+  for (int64_t k = 0; k < mine; ++k) {
+    const uint32_t slot = it % MWU_SST, parity = (it / MWU_SST) & 1u;
+    mbar_wait(&bars[slot], parity);
+    const int64_t r0 = (first + k * (int64_t)gridDim.x) * MWU_SCH;
+    const int rows = (int)((n - r0 < MWU_SCH) ? (n - r0) : MWU_SCH);
+    const double* s = buf + (size_t)slot * 3 * MWU_SCH;
+    for (int r = threadIdx.x; r < rows; r += blockDim.x) f(s[r], s[MWU_SCH + r], s[2 * MWU_SCH + r], r0 + r);
+    __syncthreads();                                   // everyone is done with this slot
+    if (threadIdx.x == 0 && k + MWU_SST < mine) issue(k + MWU_SST, slot);
+    ++it;
+  }
 }
 
 // Direction d_i = sigma * max{0, 1 - g_i/h_i} * x_i (P:279 / P:666); h_i = 0 -> 0 (Q5).

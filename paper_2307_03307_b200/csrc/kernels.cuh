@@ -28,61 +28,139 @@ __device__ __forceinline__ void set_cond(unsigned long long h, unsigned int v) {
 // =====================================================================================
 // Search controller: Alg. 3 replayed over the candidates evaluated in one HBM pass
 // =====================================================================================
+// Result slots of a search pass, per candidate j (R_*(j) index into the reduced vector):
+//   EP  sum_i u_i expm1(eta a dy_i)            (P side, expm1 form)
+//   LP  sum_i exp(eta (y_i + a dy_i - shP_j))  (P side, shifted log-sum-exp form)
+//   MX  max_i (y_i + a dy_i)
+//   EC  sum_i v_i expm1(-eta a dz_i)           (C side, expm1 form)
+//   TC  sum_i exp(-eta (z_i + a dz_i - shC_j)) (C side, shifted form; shC = s_C in DOUBLE/GRID
+//                                               passes, where it equals sum_i v_i e^{-eta a dz_i})
+//   MN  min_i (z_i + a dz_i)
+#define R_EP(j) (j)
+#define R_LP(j) (MWU_MAXC + (j))
+#define R_MX(j) (2 * MWU_MAXC + (j))
+#define R_EC(j) (3 * MWU_MAXC + (j))
+#define R_TC(j) (4 * MWU_MAXC + (j))
+#define R_MN(j) (5 * MWU_MAXC + (j))
+
 __device__ void stage_modes(Ctl* c, int j) {
   c->cea[j] = c->eta * c->cand[j];
-  c->cmP[j] = c->pSing ? CM_EXT : ((c->cea[j] * c->maxdy <= 700.0) ? CM_EXPM1 : CM_EXT);
+  if (c->pSing) c->cmP[j] = CM_EXT;
+  else if (c->cea[j] * c->maxdy <= 700.0) c->cmP[j] = CM_EXPM1;                 // Q16 branch
+  else { c->cmP[j] = CM_LSE; c->shP[j] = c->sP + c->cand[j] * c->maxdy; }        // >= max(y + a dy)
   c->cmC[j] = c->cSing ? CM_EXT : CM_EXPM1;
+  c->shC[j] = c->sC;
 }
 
-__device__ void stage_double(Ctl* c) {          // alpha, 2 alpha, 4 alpha, ...
-  double a = c->sa;
-  for (int j = 0; j < MWU_MAXC; ++j) { c->cand[j] = a; stage_modes(c, j); a = 2.0 * a; }
-  c->ncand = MWU_MAXC;
+// Doubling candidates alpha = 2^k for ascending exponents k[0..n) (alpha <- 2 alpha from 1).
+// Rows derive 2^k[j] from 2^k[j-1] by csq[j] = k[j]-k[j-1] exact squarings of expm1 / exp.
+__device__ void stage_double_exps(Ctl* c, const int* ks, int n) {
+  for (int j = 0; j < n; ++j) {
+    c->cexp[j] = ks[j];
+    c->csq[j] = j ? ks[j] - ks[j - 1] : 0;
+    c->cand[j] = ldexp(1.0, ks[j]);
+    stage_modes(c, j);
+  }
+  c->ncand = n;
+  c->ptype = PT_DOUBLE;
+  c->pa0 = c->cand[0];
 }
 
-__device__ void stage_bisect(Ctl* c) {          // dyadic tree of midpoints, BFS order
-  double lo[8], hi[8], nlo[8], nhi[8];
-  int ni = 1, n = 0;
+// Next exponents to evaluate given what is known (dk_lo passes, dk_hi stops).  By Prop. 4.2
+// (f decreasing in alpha) and the monotonicity of min(z + alpha d^(z)), every k below a
+// passing exponent passes and every k above a stopping exponent is never reached, so Alg. 3's
+// sequential outcome is decided by the first stopping exponent; the candidates are chosen to find
+// it in few passes (galloping up, then splitting the unknown gap).
+__device__ void stage_double_next(Ctl* c) {
+  int ks[MWU_MAXC], n = 0;
+  if (c->dk_hi >= (1 << 20)) {                       // no stop seen yet: gallop upward
+    const int offs[4] = {1, 2, 4, 8};
+    for (int i = 0; i < MWU_MAXC && i < 4; ++i) ks[n++] = c->dk_lo + offs[i];
+  } else {                                           // unknown exponents dk_lo+1 .. dk_hi-1
+    const int lo = c->dk_lo + 1, hi = c->dk_hi - 1, cnt = hi - lo + 1;
+    if (cnt <= MWU_MAXC) {
+      for (int k = lo; k <= hi; ++k) ks[n++] = k;
+    } else {
+      for (int i = 0; i < MWU_MAXC; ++i) {
+        const int k = lo + ((i + 1) * cnt) / (MWU_MAXC + 1);
+        if (n == 0 || k > ks[n - 1]) ks[n++] = k;
+      }
+    }
+  }
+  stage_double_exps(c, ks, n);
+}
+
+// First pass of an iteration: a window of exponents around the previous accepted step size
+// (the Table 3 caption's observation that consecutive step sizes are close, used
+// here only to choose which candidates to evaluate, not to change Alg. 3's result).
+__device__ void stage_double_first(Ctl* c) {
+  c->dk_lo = -1;
+  c->dk_hi = 1 << 20;
+  int kg = 1;
+  if (c->t > 0 && c->alpha_prev >= 1.0) kg = ilogb(c->alpha_prev);
+  int k0 = kg - 1 < 0 ? 0 : kg - 1;
+  int ks[MWU_MAXC];
+  for (int j = 0; j < MWU_MAXC; ++j) ks[j] = k0 + j;
+  stage_double_exps(c, ks, MWU_MAXC);
+}
+
+__device__ void stage_bisect(Ctl* c) {          // the 2^L - 1 midpoints of L bisection levels
+  const int Lmax = (MWU_MAXC >= 7) ? 3 : ((MWU_MAXC >= 3) ? 2 : 1);
+  const int L = c->bisect_depth < 1 ? 1 : (c->bisect_depth > Lmax ? Lmax : c->bisect_depth);
+  const int n = (1 << L) - 1;
+  // midpoints computed exactly as the sequential loop computes them, stored in ascending order
+  double lo[8], hi[8], nlo[8], nhi[8], vals[8];
+  int ni = 1, nv = 0;
   lo[0] = c->lb; hi[0] = c->ub;
-  const int L = c->bisect_depth < 1 ? 1 : (c->bisect_depth > 3 ? 3 : c->bisect_depth);
   for (int lev = 0; lev < L; ++lev) {
     int nn = 0;
     for (int k = 0; k < ni; ++k) {
       const double m = (lo[k] + hi[k]) / 2.0;
-      c->cand[n] = m; stage_modes(c, n); ++n;
+      vals[nv++] = m;
       nlo[nn] = lo[k]; nhi[nn] = m; ++nn;
       nlo[nn] = m; nhi[nn] = hi[k]; ++nn;
     }
     for (int k = 0; k < nn; ++k) { lo[k] = nlo[k]; hi[k] = nhi[k]; }
     ni = nn;
   }
+  for (int i = 1; i < nv; ++i)            // insertion sort (<= 7 values)
+    for (int k = i; k > 0 && vals[k - 1] > vals[k]; --k) { const double t = vals[k]; vals[k] = vals[k - 1]; vals[k - 1] = t; }
+  for (int k = 0; k < n; ++k) { c->cand[k] = vals[k]; stage_modes(c, k); }
   c->ncand = n;
+  c->ptype = PT_GRID;
+  c->pa0 = c->lb;
+  c->pdelta = (c->ub - c->lb) / (double)(1 << L);
 }
 
-// eta*Psi and eta*Phi of candidate j (P:719-720, P:322 singletons, Q12, Q16)
+// eta*Psi and eta*Phi of candidate j (P:719-720, P:322 singletons, Q12, Q16).  The shifted
+// forms use the pass's shift sh: eta*Psi = eta(sh - s_P) + log(sum exp(eta(t - sh))) - log S_P,
+// eta*Phi = eta(sh - s_C) - log(sum exp(-eta(t - sh))) + log S_C, identical in value to the
+// oracle's max/min-shifted forms; a sum that underflowed asks for an exact-shift re-pass.
 __device__ void eval_cand(const Ctl* c, int j, const double* res, double& psi, double& phi,
                           int& needP, int& needC) {
   const double ea = c->cea[j];
   needP = needC = 0;
   psi = phi = 0.0;
   if (c->pSing) psi = ea * c->dyS;
-  else if (c->cmP[j] == CM_EXPM1) psi = log1p(res[j] / c->SP);
-  else if (c->cmP[j] == CM_LSE) psi = c->eta * (res[MWU_MAXC + j] - c->sP) + log(res[j]) - log(c->SP);
+  else if (c->cmP[j] == CM_EXPM1) psi = log1p(res[R_EP(j)] / c->SP);
+  else if (c->cmP[j] == CM_LSE && res[R_LP(j)] > 1e-280)
+    psi = c->eta * (c->shP[j] - c->sP) + log(res[R_LP(j)]) - log(c->SP);
   else needP = 1;
   if (c->cSing) phi = ea * c->dzS;
-  else if (c->cmC[j] == CM_EXPM1) {
-    const double e = res[2 * MWU_MAXC + j] / c->SC;
-    if (e >= -0.5) phi = -log1p(e); else needC = 1;
-  } else if (c->cmC[j] == CM_LSE) {
-    phi = c->eta * (res[3 * MWU_MAXC + j] - c->sC) - log(res[2 * MWU_MAXC + j]) + log(c->SC);
-  } else needC = 1;
+  else {
+    const double e = (c->cmC[j] == CM_EXPM1) ? res[R_EC(j)] / c->SC : -1.0;
+    if (c->cmC[j] == CM_EXPM1 && e >= -0.5) phi = -log1p(e);
+    else if (c->cmC[j] != CM_EXT && res[R_TC(j)] > 1e-280)
+      phi = c->eta * (c->shC[j] - c->sC) - log(res[R_TC(j)]) + log(c->SC);
+    else needC = 1;
+  }
 }
 
 __device__ __forceinline__ double cand_mx(const Ctl* c, int j, const double* res) {
-  return c->pSing ? (c->yS + c->cand[j] * c->dyS) : res[MWU_MAXC + j];
+  return c->pSing ? (c->yS + c->cand[j] * c->dyS) : res[R_MX(j)];
 }
 __device__ __forceinline__ double cand_mn(const Ctl* c, int j, const double* res) {
-  return c->cSing ? (c->zS + c->cand[j] * c->dzS) : res[3 * MWU_MAXC + j];
+  return c->cSing ? (c->zS + c->cand[j] * c->dzS) : res[R_MN(j)];
 }
 
 __device__ void accept_alpha(Ctl* c, double a, double mx, double mn) {
@@ -94,15 +172,63 @@ __device__ void accept_alpha(Ctl* c, double a, double mx, double mn) {
   if (a < 1.0) { c->status = ST_INFEASIBLE; c->reason = R_ALPHA_LT_1; }
 }
 
-// res layout: [0,8) sums P side, [8,16) max(y + a dy), [16,24) sums C side, [24,32) min(z + a dz)
+// res layout: see R_* above
 __device__ void search_controller(Ctl* c, const double* res) {
   c->passes_total++;
-  for (int guard = 0; guard < 4096; ++guard) {
-    if (c->sphase == SP_FIXED) { accept_alpha(c, c->cand[0], cand_mx(c, 0, res), cand_mn(c, 0, res)); return; }
-    double need;
-    if (c->sphase == SP_DOUBLE) {
-      need = c->sa;
+  if (c->sphase == SP_FIXED) { accept_alpha(c, c->cand[0], cand_mx(c, 0, res), cand_mn(c, 0, res)); return; }
+  if (c->sphase == SP_DOUBLE) {
+    // classify the evaluated exponents (ascending): pass = f >= 1 and min(z + a dz) < 1
+    int lse_j = -1;
+    for (int j = 0; j < c->ncand; ++j) {
+      const int k = c->cexp[j];
+      if (k <= c->dk_lo || k >= c->dk_hi) continue;             // outcome already implied
+      double psi, phi; int nP, nC;
+      eval_cand(c, j, res, psi, phi, nP, nC);
+      if (nP || nC) { if (lse_j < 0) lse_j = j; continue; }
+      const double mxj = cand_mx(c, j, res), mnj = cand_mn(c, j, res);
+      const bool ok = phi >= psi;                                  // eq:b4b_conv
+      if (ok && mnj < 1.0) { c->dk_lo = k; c->ok_mx = mxj; c->ok_mn = mnj; }
+      else { c->dk_hi = k; c->hi_exit = ok ? 1 : 0; c->hi_mx = mxj; c->hi_mn = mnj; }
+    }
+    if (lse_j >= 0 && c->cexp[lse_j] > c->dk_lo && c->cexp[lse_j] < c->dk_hi) {
+      // Q16: re-evaluate this exponent with the exact max / min shift
+      double psi, phi; int nP, nC;
+      eval_cand(c, lse_j, res, psi, phi, nP, nC);
+      const double mxj = cand_mx(c, lse_j, res), mnj = cand_mn(c, lse_j, res);
+      const int k = c->cexp[lse_j];
+      const int keepP = c->cmP[lse_j];
+      const double kshP = c->shP[lse_j];
+      c->cand[0] = ldexp(1.0, k); c->cea[0] = c->eta * c->cand[0]; c->cexp[0] = k; c->csq[0] = 0;
+      c->cmP[0] = c->pSing ? CM_EXT : (nP ? CM_LSE : keepP); c->shP[0] = nP ? mxj : kshP;
+      c->cmC[0] = c->cSing ? CM_EXT : (nC ? CM_LSE : CM_EXPM1); c->shC[0] = nC ? mnj : c->sC;
+      c->ncand = 1; c->ptype = PT_LIST; c->sactive = 1;
+      return;
+    }
+    // the literal loop stops at the first stopping exponent k* = dk_hi (alpha = 2^k*) after k*+1
+    // evaluations; the cap max_evals stops it earlier at alpha = 2^(max_evals-1)
+    const int cap_k = c->max_evals - 1;
+    if (c->dk_lo >= cap_k || (c->dk_hi == c->dk_lo + 1 && c->dk_hi > cap_k)) {
+      c->evals = c->max_evals; c->evals_total += c->max_evals;
+      if (c->dk_lo == cap_k) { accept_alpha(c, ldexp(1.0, cap_k), c->ok_mx, c->ok_mn); return; }
+      c->sphase = SP_FIXED; c->ncand = 1; c->cand[0] = ldexp(1.0, cap_k); c->ptype = PT_LIST;   // shifts only
+      c->cea[0] = c->eta * c->cand[0]; c->cmP[0] = CM_EXT; c->cmC[0] = CM_EXT; c->sactive = 1;
+      return;
+    }
+    if (c->dk_hi == c->dk_lo + 1) {
+      const int ks = c->dk_hi;
+      c->evals = ks + 1; c->evals_total += ks + 1;
+      if (c->hi_exit) { accept_alpha(c, ldexp(1.0, ks), c->hi_mx, c->hi_mn); return; }
+      c->sphase = SP_BISECT; c->lb = ldexp(1.0, ks - 1); c->ub = ldexp(1.0, ks);
+      c->lb_mx = c->ok_mx; c->lb_mn = c->ok_mn;
     } else {
+      stage_double_next(c);
+      c->sactive = 1;
+      return;
+    }
+  }
+  for (int guard = 0; guard < 4096; ++guard) {
+    double need;
+    {
       const double thr = c->tol_prose ? c->eps : (1.0 - c->eps);         // Q9
       if (!((c->ub - c->lb) > thr * c->lb && c->evals < c->max_evals)) {
         accept_alpha(c, c->lb, c->lb_mx, c->lb_mn);                         // return lb
@@ -113,37 +239,28 @@ __device__ void search_controller(Ctl* c, const double* res) {
     int j = -1;
     for (int k = 0; k < c->ncand; ++k) if (c->cand[k] == need) { j = k; break; }
     if (j < 0) {                                                            // not evaluated yet
-      if (c->sphase == SP_DOUBLE) stage_double(c); else stage_bisect(c);
+      stage_bisect(c);
       c->sactive = 1;
       return;
     }
     double psi, phi; int nP, nC;
     eval_cand(c, j, res, psi, phi, nP, nC);
     const double mxj = cand_mx(c, j, res), mnj = cand_mn(c, j, res);
-    if (nP || nC) {                                                         // Q16 shifted form
+    if (nP || nC) {                          // Q16 shifted form with the exact max / min shift
+      const int keepP = c->cmP[j], keepC = c->cmC[j];
+      const double kshP = c->shP[j];
       c->cand[0] = need; c->cea[0] = c->eta * need;
-      c->cmP[0] = c->pSing ? CM_EXT : (nP ? CM_LSE : CM_EXPM1); c->shP[0] = mxj;
-      c->cmC[0] = c->cSing ? CM_EXT : (nC ? CM_LSE : CM_EXPM1); c->shC[0] = mnj;
+      c->cmP[0] = c->pSing ? CM_EXT : (nP ? CM_LSE : keepP); c->shP[0] = nP ? mxj : kshP;
+      c->cmC[0] = c->cSing ? CM_EXT : (nC ? CM_LSE : CM_EXPM1); c->shC[0] = nC ? mnj : c->sC;
       c->ncand = 1;
+      c->ptype = PT_LIST;
       c->sactive = 1;
       return;
     }
     const bool ok = phi >= psi;                                             // eq:b4b_conv
     c->evals++;
     c->evals_total++;
-    if (c->sphase == SP_DOUBLE) {
-      if (!ok) {
-        c->sphase = SP_BISECT; c->lb = c->sa / 2.0; c->ub = c->sa;
-        c->lb_mx = c->ok_mx; c->lb_mn = c->ok_mn;
-        continue;
-      }
-      c->ok_mx = mxj; c->ok_mn = mnj;
-      if (mnj >= 1.0) { accept_alpha(c, c->sa, mxj, mnj); return; }       // early exit P:813-815
-      if (c->evals >= c->max_evals) { accept_alpha(c, c->sa, mxj, mnj); return; }
-      c->sa = 2.0 * c->sa;
-    } else {
-      if (ok) { c->lb = need; c->lb_mx = mxj; c->lb_mn = mnj; } else { c->ub = need; }
-    }
+    if (ok) { c->lb = need; c->lb_mx = mxj; c->lb_mn = mnj; } else { c->ub = need; }
   }
   c->status = ST_INFEASIBLE; c->reason = R_ALPHA_LT_1; c->sactive = 0;   // unreachable guard
 }
@@ -169,11 +286,11 @@ __device__ void finalize(Ctl* c, int action, const double* r) {
       if (action == A_STEP_DONE + 100) c->maxdy = r[0];
       c->evals = 0;
       if (c->fixed_alpha > 0.0) {
-        c->sphase = SP_FIXED; c->ncand = 1; c->cand[0] = c->fixed_alpha;
+        c->sphase = SP_FIXED; c->ncand = 1; c->cand[0] = c->fixed_alpha; c->ptype = PT_LIST;
         c->cea[0] = c->eta * c->fixed_alpha; c->cmP[0] = CM_EXT; c->cmC[0] = CM_EXT;
       } else {
         c->sphase = SP_DOUBLE; c->sa = 1.0;                                 // alpha <- 1
-        stage_double(c);
+        stage_double_first(c);
       }
       c->sactive = 1;
       set_cond(c->h_search, 1u);
@@ -327,6 +444,7 @@ __global__ void __launch_bounds__(MWU_NT) seg_main(SegView sv, Item item, Ep ep,
     const int64_t i0 = sv.rowptr[r0];
     const int64_t nit = sv.rowptr[r1] - i0;                              // <= 2*TILE
     // stage item values (coalesced index loads, independent gathers)
+#pragma unroll 8
     for (int64_t j = threadIdx.x; j < nit; j += MWU_NT) vals[j] = item(i0 + j, scale);
     __syncthreads();
     // group size: power of two ~ average row length, 1..32
@@ -420,24 +538,45 @@ struct EpColumn {
 // =====================================================================================
 // MATCH / BMATCH column (P = M, C = (1/M)1^T): g_e = w_p[r(src)] + w_p[r(dst)] (M^T),
 // h_e = 1/M, d_e; lazy x update; reduce max d, sum(d/M).
-__global__ void __launch_bounds__(MWU_NT) col_match(int64_t E, const int32_t* __restrict__ srow,
+__global__ void __launch_bounds__(MWU_NT, 2) col_match(int64_t E, const int32_t* __restrict__ srow,
                                                     const int32_t* __restrict__ drow, const double* __restrict__ u,
                                                     double* __restrict__ x, double* __restrict__ d,
                                                     double* gdbg, double* hdbg, Ctl* c, double* part,
                                                     unsigned int* counter) {
   if (c->status != ST_RUNNING) return;
-  const double SP = c->SP, invB = c->invB, sigma = c->sigma, ap = c->alpha_prev;
+  const double rSP = 1.0 / c->SP, invB = c->invB, sigma = c->sigma, ap = c->alpha_prev;
   const int apply = c->apply_prev;
   double acc[2] = {-INFINITY, 0.0};
-  for (int64_t e = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; e < E; e += (int64_t)gridDim.x * MWU_NT) {
-    double xe = x[e];
-    if (apply) { xe = xe + ap * d[e]; x[e] = xe; }
-    const double g = __ldg(u + __ldg(srow + e)) / SP + __ldg(u + __ldg(drow + e)) / SP;
-    const double de = mwu_direction(g, invB, xe, sigma);
-    d[e] = de;
-    if (gdbg) { gdbg[e] = g; hdbg[e] = invB; }
-    acc[0] = fmax(acc[0], de);
-    acc[1] += invB * de;
+  constexpr int U = 2;   // edges per thread per trip: all independent loads issued before use
+  const int64_t stride = (int64_t)gridDim.x * MWU_NT;
+  for (int64_t e0 = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; e0 < E; e0 += U * stride) {
+    double xe[U], dp[U], us[U], ud[U];
+    int32_t sr[U], dr[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t e = e0 + k * stride;
+      if (e < E) {
+        xe[k] = x[e];
+        dp[k] = apply ? d[e] : 0.0;
+        sr[k] = __ldg(srow + e);
+        dr[k] = __ldg(drow + e);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (e0 + k * stride < E) { us[k] = __ldg(u + sr[k]); ud[k] = __ldg(u + dr[k]); }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t e = e0 + k * stride;
+      if (e >= E) break;
+      if (apply) { xe[k] = xe[k] + ap * dp[k]; x[e] = xe[k]; }   // lazy x += alpha d
+      const double g = us[k] * rSP + ud[k] * rSP;                 // M^T w_p
+      const double de = mwu_direction(g, invB, xe[k], sigma);
+      d[e] = de;
+      if (gdbg) { gdbg[e] = g; hdbg[e] = invB; }
+      acc[0] = fmax(acc[0], de);
+      acc[1] += invB * de;
+    }
   }
   const int ops[2] = {OP_MAX, OP_SUM};
   reduce_and_finalize<2>(acc, ops, part, counter, c, A_COL);
@@ -445,36 +584,58 @@ __global__ void __launch_bounds__(MWU_NT) col_match(int64_t E, const int32_t* __
 
 // DENSEST column (P = O/D, C = W): for edge e, slots s = 2e+b: g_s = (1/D) w_p[r_b] (O^T),
 // h_s = w_c[e] (W^T), d_s (sigma = 1/(2 eta)), and d^(z)_e = d_2e + d_2e+1 (W d) fused.
-__global__ void __launch_bounds__(MWU_NT) col_densest(int64_t E, const int32_t* __restrict__ srow,
+__global__ void __launch_bounds__(MWU_NT, 2) col_densest(int64_t E, const int32_t* __restrict__ srow,
                                                       const int32_t* __restrict__ drow, const double* __restrict__ u,
                                                       const double* __restrict__ v, double* __restrict__ x,
                                                       double* __restrict__ d, double* __restrict__ dz,
                                                       double* gdbg, double* hdbg, Ctl* c, double* part,
                                                       unsigned int* counter) {
   if (c->status != ST_RUNNING) return;
-  const double SP = c->SP, SC = c->SC, invD = c->invB, sigma = c->sigma, ap = c->alpha_prev;
+  const double rSP = 1.0 / c->SP, rSC = 1.0 / c->SC, invD = c->invB, sigma = c->sigma, ap = c->alpha_prev;
   const int apply = c->apply_prev;
   double acc[2] = {-INFINITY, 0.0};
   double2* x2 = reinterpret_cast<double2*>(x);
   double2* d2 = reinterpret_cast<double2*>(d);
-  for (int64_t e = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; e < E; e += (int64_t)gridDim.x * MWU_NT) {
-    double2 xe = x2[e];
-    if (apply) {
-      const double2 dp = d2[e];
-      xe.x = xe.x + ap * dp.x;
-      xe.y = xe.y + ap * dp.y;
-      x2[e] = xe;
+  constexpr int U = 2;   // edges per thread per trip: all independent loads issued before use
+  const int64_t stride = (int64_t)gridDim.x * MWU_NT;
+  for (int64_t e0 = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; e0 < E; e0 += U * stride) {
+    double2 xe[U], dp[U];
+    double vv[U], us[U], ud[U];
+    int32_t sr[U], dr[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t e = e0 + k * stride;
+      if (e < E) {
+        xe[k] = x2[e];
+        dp[k] = apply ? d2[e] : make_double2(0.0, 0.0);
+        vv[k] = __ldg(v + e);
+        sr[k] = __ldg(srow + e);
+        dr[k] = __ldg(drow + e);
+      }
     }
-    const double h = __ldg(v + e) / SC;
-    const double g0 = invD * (__ldg(u + __ldg(srow + e)) / SP);
-    const double g1 = invD * (__ldg(u + __ldg(drow + e)) / SP);
-    double2 de;
-    de.x = mwu_direction(g0, h, xe.x, sigma);
-    de.y = mwu_direction(g1, h, xe.y, sigma);
-    d2[e] = de;
-    dz[e] = de.x + de.y;
-    if (gdbg) { gdbg[2 * e] = g0; gdbg[2 * e + 1] = g1; hdbg[2 * e] = h; hdbg[2 * e + 1] = h; }
-    acc[0] = fmax(acc[0], fmax(de.x, de.y));
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (e0 + k * stride < E) { us[k] = __ldg(u + sr[k]); ud[k] = __ldg(u + dr[k]); }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t e = e0 + k * stride;
+      if (e >= E) break;
+      if (apply) {                                               // lazy x += alpha d
+        xe[k].x = xe[k].x + ap * dp[k].x;
+        xe[k].y = xe[k].y + ap * dp[k].y;
+        x2[e] = xe[k];
+      }
+      const double h = vv[k] * rSC;
+      const double g0 = invD * (us[k] * rSP);
+      const double g1 = invD * (ud[k] * rSP);
+      double2 de;
+      de.x = mwu_direction(g0, h, xe[k].x, sigma);
+      de.y = mwu_direction(g1, h, xe[k].y, sigma);
+      d2[e] = de;
+      dz[e] = de.x + de.y;
+      if (gdbg) { gdbg[2 * e] = g0; gdbg[2 * e + 1] = g1; hdbg[2 * e] = h; hdbg[2 * e + 1] = h; }
+      acc[0] = fmax(acc[0], fmax(de.x, de.y));
+    }
   }
   const int ops[2] = {OP_MAX, OP_SUM};
   reduce_and_finalize<2>(acc, ops, part, counter, c, A_COL);
@@ -513,6 +674,8 @@ __global__ void __launch_bounds__(MWU_NT) pair_sum(int64_t E, const double* __re
 // =====================================================================================
 // Row kernels: search pass and update (P rows then C rows as one index space)
 // =====================================================================================
+constexpr size_t kSearchSmem = (size_t)MWU_SST * 3 * MWU_SCH * sizeof(double);
+
 // One HBM pass evaluating the staged candidates (P:716-727 on cached vectors).
 __global__ void __launch_bounds__(MWU_NT) search_pass(int64_t mP, const double* __restrict__ y,
                                                       const double* __restrict__ dy, const double* __restrict__ u,
@@ -524,52 +687,83 @@ __global__ void __launch_bounds__(MWU_NT) search_pass(int64_t mP, const double* 
     return;
   }
   __shared__ double s_a[MWU_MAXC], s_ea[MWU_MAXC], s_shP[MWU_MAXC], s_shC[MWU_MAXC];
-  __shared__ int s_mP[MWU_MAXC], s_mC[MWU_MAXC];
+  __shared__ int s_mP[MWU_MAXC], s_mC[MWU_MAXC], s_sq[MWU_MAXC];
   if (threadIdx.x < MWU_MAXC) {
     const int j = threadIdx.x;
     s_a[j] = c->cand[j]; s_ea[j] = c->cea[j]; s_shP[j] = c->shP[j]; s_shC[j] = c->shC[j];
-    s_mP[j] = c->cmP[j]; s_mC[j] = c->cmC[j];
+    s_mP[j] = c->cmP[j]; s_mC[j] = c->cmC[j]; s_sq[j] = c->csq[j];
   }
   __syncthreads();
-  const int nc = c->ncand;
+  const int nc = c->ncand, pt = c->ptype;
   const double eta = c->eta, neta = -c->eta;
-  double acc[4 * MWU_MAXC];
+  // one transcendental per row and pass (per side): candidates follow by exact identities
+  //   doubling  a -> 2a : expm1(2x) = e (e + 2),           exp(2x) = q^2
+  //   grid  a -> a + delta: expm1(x + w) = e + e_w + e e_w, exp(x + w) = q q_w
+  const double ea0 = eta * c->pa0, ead = eta * c->pdelta;
+  double acc[6 * MWU_MAXC];
 #pragma unroll
   for (int j = 0; j < MWU_MAXC; ++j) {
-    acc[j] = 0.0; acc[MWU_MAXC + j] = -INFINITY; acc[2 * MWU_MAXC + j] = 0.0; acc[3 * MWU_MAXC + j] = INFINITY;
+    acc[R_EP(j)] = 0.0; acc[R_LP(j)] = 0.0; acc[R_MX(j)] = -INFINITY;
+    acc[R_EC(j)] = 0.0; acc[R_TC(j)] = 0.0; acc[R_MN(j)] = INFINITY;
   }
-  const int64_t stride = (int64_t)gridDim.x * MWU_NT;
-  const int64_t tid = (int64_t)blockIdx.x * MWU_NT + threadIdx.x;
-  for (int64_t i = tid; i < mP; i += stride) {
-    const double yi = y[i], di = dy[i], ui = u[i];
+  extern __shared__ __align__(128) double sbuf[];
+  __shared__ __align__(8) uint64_t bars[MWU_SST];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < MWU_SST; ++s) mbar_init(&bars[s], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  uint32_t it = 0;
+  stream_rows3(y, dy, u, mP, sbuf, bars, it, [&](double yi, double di, double ui, int64_t) {
+    double em = 0.0, emd = 0.0;
+    if (pt != PT_LIST) em = expm1(ea0 * di);
+    if (pt == PT_GRID) emd = expm1(ead * di);
 #pragma unroll
     for (int j = 0; j < MWU_MAXC; ++j) {
       if (j < nc) {
+        if (pt == PT_DOUBLE) { for (int s = 0; s < s_sq[j]; ++s) em = em * (em + 2.0); }
+        else if (pt == PT_GRID) em = em + emd + em * emd;
+        else if (s_mP[j] == CM_EXPM1) em = expm1(s_ea[j] * di);
         const double t = yi + s_a[j] * di;
-        acc[MWU_MAXC + j] = fmax(acc[MWU_MAXC + j], t);
-        if (s_mP[j] == CM_EXPM1) acc[j] += ui * expm1(s_ea[j] * di);
-        else if (s_mP[j] == CM_LSE) acc[j] += exp(eta * (t - s_shP[j]));
+        acc[R_MX(j)] = fmax(acc[R_MX(j)], t);
+        if (s_mP[j] == CM_EXPM1) acc[R_EP(j)] = __fma_rn(ui, em, acc[R_EP(j)]);   // sums: any order
+        else if (s_mP[j] == CM_LSE) acc[R_LP(j)] += exp(eta * (t - s_shP[j]));
       }
     }
-  }
-  for (int64_t i = tid; i < mC; i += stride) {
-    const double zi = z[i], di = dz[i], vi = v[i];
+  });
+  stream_rows3(z, dz, v, mC, sbuf, bars, it, [&](double zi, double di, double vi, int64_t) {
+    double em = 0.0, q = 1.0, emd = 0.0, qd = 1.0;
+    if (pt != PT_LIST) {
+      const double xa = -(ea0 * di);
+      if (xa >= -0.6931471805599453) { em = expm1(xa); q = 1.0 + em; } else { q = exp(xa); em = q - 1.0; }
+      if (pt == PT_GRID) {
+        const double xd = -(ead * di);
+        if (xd >= -0.6931471805599453) { emd = expm1(xd); qd = 1.0 + emd; } else { qd = exp(xd); emd = qd - 1.0; }
+      }
+    }
 #pragma unroll
     for (int j = 0; j < MWU_MAXC; ++j) {
       if (j < nc) {
+        if (pt == PT_DOUBLE) { for (int s = 0; s < s_sq[j]; ++s) { em = em * (em + 2.0); q = q * q; } }
+        else if (pt == PT_GRID) { em = em + emd + em * emd; q = q * qd; }
+        else if (s_mC[j] == CM_EXPM1) {
+          const double xa = -(s_ea[j] * di);
+          if (xa >= -0.6931471805599453) { em = expm1(xa); q = 1.0 + em; } else { q = exp(xa); em = q - 1.0; }
+        }
         const double t = zi + s_a[j] * di;
-        acc[3 * MWU_MAXC + j] = fmin(acc[3 * MWU_MAXC + j], t);
-        if (s_mC[j] == CM_EXPM1) acc[2 * MWU_MAXC + j] += vi * expm1(-(s_ea[j] * di));
-        else if (s_mC[j] == CM_LSE) acc[2 * MWU_MAXC + j] += exp(neta * (t - s_shC[j]));
+        acc[R_MN(j)] = fmin(acc[R_MN(j)], t);
+        if (s_mC[j] == CM_EXPM1) { acc[R_EC(j)] = __fma_rn(vi, em, acc[R_EC(j)]); acc[R_TC(j)] = __fma_rn(vi, q, acc[R_TC(j)]); }
+        else if (s_mC[j] == CM_LSE) acc[R_TC(j)] += exp(neta * (t - s_shC[j]));
       }
     }
+  });
+  int ops[6 * MWU_MAXC];
+#pragma unroll
+  for (int j = 0; j < MWU_MAXC; ++j) {
+    ops[R_EP(j)] = OP_SUM; ops[R_LP(j)] = OP_SUM; ops[R_MX(j)] = OP_MAX;
+    ops[R_EC(j)] = OP_SUM; ops[R_TC(j)] = OP_SUM; ops[R_MN(j)] = OP_MIN;
   }
-  const int ops[4 * MWU_MAXC] = {
-      OP_SUM, OP_SUM, OP_SUM, OP_SUM, OP_SUM, OP_SUM, OP_SUM, OP_SUM,
-      OP_MAX, OP_MAX, OP_MAX, OP_MAX, OP_MAX, OP_MAX, OP_MAX, OP_MAX,
-      OP_SUM, OP_SUM, OP_SUM, OP_SUM, OP_SUM, OP_SUM, OP_SUM, OP_SUM,
-      OP_MIN, OP_MIN, OP_MIN, OP_MIN, OP_MIN, OP_MIN, OP_MIN, OP_MIN};
-  reduce_and_finalize<4 * MWU_MAXC>(acc, ops, part, counter, c, A_SEARCH);
+  reduce_and_finalize<6 * MWU_MAXC>(acc, ops, part, counter, c, A_SEARCH);
 }
 
 // y += alpha d^(y), z += alpha d^(z) fused with u = exp(eta (y - s_P)),

@@ -4,6 +4,7 @@
 #include "kernels.cuh"
 #include "storage.cuh"
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -101,6 +102,7 @@ namespace {
 template <class T>
 T* dalloc(mwu_ctx* c, int64_t n) {
   if (n <= 0) n = 1;
+  n += 4;  // padding: 16-byte bulk copies of a ragged tail stay inside the allocation
   void* p = nullptr;
   CK(cudaMalloc(&p, (size_t)n * sizeof(T)));
   c->allocs.push_back(p);
@@ -275,6 +277,7 @@ void init_ctx_common(mwu_ctx* c, const mwu_options* opt) {
   CK(cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st));
   c->part = dalloc<double>(c, (int64_t)c->grid_max * MWU_SLOTS);
   c->counter = dalloc<unsigned int>(c, 1);
+  CK(cudaFuncSetAttribute(search_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSearchSmem));
   CK(cudaMemsetAsync(c->counter, 0, sizeof(unsigned int), c->st));
   CK(cudaEventCreate(&c->ev0));
   CK(cudaEventCreate(&c->ev1));
@@ -568,8 +571,10 @@ void enqueue_forward(mwu_ctx* c, cudaStream_t st, const double* in, double* oy, 
 }
 
 void enqueue_search(mwu_ctx* c, cudaStream_t st) {
-  search_pass<<<rows_grid(c, c->mP + c->mC), MWU_NT, 0, st>>>(c->mP, c->y, c->dy, c->u, c->mC, c->z, c->dz, c->v,
-                                                              c->ctl, c->part, c->counter);
+  const int64_t chunks = (std::max(c->mP, c->mC) + MWU_SCH - 1) / MWU_SCH;
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>(2 * c->sms, chunks));   // 2 CTAs / SM
+  search_pass<<<g, MWU_NT, kSearchSmem, st>>>(c->mP, c->y, c->dy, c->u, c->mC, c->z, c->dz, c->v,
+                                              c->ctl, c->part, c->counter);
   c->launches++;
 }
 
