@@ -105,6 +105,10 @@ typedef struct {
   int device;            /* CUDA device ordinal; -1 = current device                             */
   int world, rank;       /* multi-GPU: number of ranks and this rank (1, 0 for one GPU)          */
   const void *nccl_id;   /* 128-byte ncclUniqueId from mwu_get_unique_id on rank 0 (world > 1)   */
+  int deterministic;     /* 1: every reduction in a fixed order (run-to-run bit-identical); 0     */
+                         /* (default): the forward product of graph kinds is scattered with fp64 */
+                         /* atomics into the L2-resident vertex vector (summation order varies   */
+                         /* run to run at the 1e-16 level)                          */
 } mwu_options;
 
 typedef struct {

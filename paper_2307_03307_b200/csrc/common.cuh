@@ -11,12 +11,16 @@
 #include <math.h>
 
 #define MWU_NT 256            // threads per block for every kernel
-#define MWU_MAXC 4            // step-search candidates evaluated per HBM pass
-#define MWU_SLOTS 24          // reduction slots per block partial (6 * MAXC)
+#define MWU_MAXC 8            // step-search candidates evaluated per HBM pass
+#define MWU_SLOTS 48          // reduction slots per block partial (6 * MAXC)
+#define MWU_CT 512            // edges per column tile (compacted covering-row records)
 #define MWU_TILE 2048         // items per seg tile (a tile loads <= 2*TILE items into smem)
 #define MWU_LCH 8192          // items per chunk of a long row (deg > TILE)
 
 namespace mwu {
+
+constexpr int kColEdges = MWU_CT / MWU_NT;         // edges per thread per column tile
+constexpr int kWarpSeg = MWU_CT / (MWU_NT / 32);   // edges (and record slots) per warp per tile
 
 enum Status : int { ST_RUNNING = 0, ST_FEASIBLE = 1, ST_INFEASIBLE = 2, ST_ITER_LIMIT = 3 };
 enum Reason : int { R_NONE = 0, R_MAXD_ZERO = 1, R_ALPHA_LT_1 = 2, R_EMPTY_COVER = 3, R_ITER_LIMIT = 4, R_MIN_Z = 5 };
@@ -24,7 +28,7 @@ enum RedOp : int { OP_SUM = 0, OP_MAX = 1, OP_MIN = 2 };
 // candidate evaluation modes of one side in a search pass (DESIGN.md §3 Q16)
 enum CandMode : int { CM_EXPM1 = 0, CM_LSE = 1, CM_EXT = 2 };
 // search phases (Alg. 3)
-enum SPhase : int { SP_DOUBLE = 0, SP_BISECT = 1, SP_DONE = 2, SP_FIXED = 3 };
+enum SPhase : int { SP_DOUBLE = 0, SP_BISECT = 1, SP_DONE = 2, SP_FIXED = 3, SP_TCFIX = 4 };
 // candidate layout of a search pass: explicit list, doubling a0*2^j, bisection grid a0 + k*delta
 enum PType : int { PT_LIST = 0, PT_DOUBLE = 1, PT_GRID = 2 };
 
@@ -40,6 +44,8 @@ enum Action : int {
   A_INIT_EXT = 7,   // init: shifts s_P = max y, s_C = min z
   A_INIT_W = 8,     // init: S_P, S_C, termination test at t = 0
   A_SUM = 9,        // generic: store the reduced slots in ctl->scratch
+  A_COL_FAST = 10,  // fast densest column: max d, inactive covering aggregate (mzi, Vi)
+  A_VI_EXACT = 11,  // exact inactive aggregate at shift mzi (rare path)
 };
 
 // Device-resident control block of one probe (one per context).
@@ -50,6 +56,9 @@ struct Ctl {
   int32_t pSing, cSing;                // side is the embedded singleton row
   int32_t mode;                        // 0 mixed, 1 pure packing, 2 pure covering
   int32_t tol_prose, max_evals, bisect_depth, use_graph;
+  int32_t lazyC, pad0_;                // covering rows of the fast densest path: z updated lazily in
+                                       // the column kernel, weights v recomputed from z, S_C carried
+                                       // from the accepted alpha's search pass
   // ---- iteration state
   int64_t t;                           // completed MWU iterations
   int64_t iter_stop;                   // graph loop stops when t reaches this (benchmarks)
@@ -65,6 +74,11 @@ struct Ctl {
   int32_t ncand, evals;                // candidates in this pass; f evaluations this iteration
   double sa, lb, ub;                   // doubling alpha, bisection bracket
   double lb_mx, lb_mn, ok_mx, ok_mn;   // ext values of lb / the last accepted doubling alpha
+  double lb_tc, lb_sh, ok_tc, ok_sh, hi_tc, hi_sh;   // covering-side shifted sums (and their shifts)
+  double acc_tc, acc_sh;               // of the accepted alpha (lazyC: S_C of the next iterate)
+  int32_t vi_exact, pad4_;             // lazyC: the inactive aggregate needs the exact pass
+  double mzi, Vi;                      // lazyC: inactive covering rows (d^(z) = 0): min z and
+                                       // sum exp(-eta (z - mzi)) (candidate independent)
   double fixed_alpha;
   int32_t ptype, pad2_;                // pass layout: PT_LIST, PT_DOUBLE (a0 2^j), PT_GRID (a0 + k delta)
   double pa0, pdelta;
@@ -92,10 +106,10 @@ __device__ __forceinline__ double red_combine(int op, double a, double b) {
   return op == OP_SUM ? __dadd_rn(a, b) : (op == OP_MAX ? fmax(a, b) : fmin(a, b));
 }
 
-// Reduce NS per-thread values across the block and write this block's partial row.
-// ops: compile-time-unknown but warp-uniform op per slot.
+// Reduce NS per-thread values across the block and write this block's partials into slots
+// [slot0, slot0 + NS) of its partial row.  ops: warp-uniform op per slot.
 template <int NS>
-__device__ __forceinline__ void block_partials(double (&v)[NS], const int* ops, double* part) {
+__device__ __forceinline__ void block_partials(const double (&v)[NS], const int* ops, double* part, int slot0 = 0) {
   __shared__ double sh[MWU_NT / 32][MWU_SLOTS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -110,17 +124,18 @@ __device__ __forceinline__ void block_partials(double (&v)[NS], const int* ops, 
     const int s = threadIdx.x;
     double a = sh[0][s];
     for (int w = 1; w < MWU_NT / 32; ++w) a = red_combine(ops[s], a, sh[w][s]);
-    part[(size_t)blockIdx.x * MWU_SLOTS + s] = a;
+    part[(size_t)blockIdx.x * MWU_SLOTS + slot0 + s] = a;
   }
+  __syncthreads();   // sh may be reused by the next call
 }
 
-// Returns true in the last block to finish; in that block out[0..NS) holds the grid result
-// (combined over blocks 0..gridDim.x-1 in a fixed order).  Must be called by all threads.
-template <int NS>
-__device__ __forceinline__ bool last_block_reduce(const int* ops, const double* part,
-                                                  unsigned int* counter, double (&out)[NS]) {
+// Returns true in the last block to finish; there res[0..nslots) (shared memory) holds the grid
+// result of every slot, combined over blocks 0..gridDim.x-1 in a fixed order.  Must be called
+// by all threads; ops[s] is the op of slot s.
+__device__ __forceinline__ bool last_block_combine(const int* ops, int nslots, const double* part,
+                                                   unsigned int* counter, double* res) {
   __shared__ int am_last;
-  __shared__ double sh2[MWU_NT][1];
+  __shared__ double sh2[MWU_NT];
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -130,19 +145,18 @@ __device__ __forceinline__ bool last_block_reduce(const int* ops, const double* 
   __syncthreads();
   if (!am_last) return false;
   __threadfence();
-  const int L = MWU_NT / NS;              // lanes per slot
-  const int s = threadIdx.x % NS, k = threadIdx.x / NS;
+  const int L = MWU_NT / nslots;          // lanes per slot
+  const int s = threadIdx.x % nslots, k = threadIdx.x / nslots;
   double a = red_identity(ops[s]);
   if (k < L)
     for (unsigned int b = k; b < gridDim.x; b += L)
       a = red_combine(ops[s], a, __ldcg(part + (size_t)b * MWU_SLOTS + s));
-  sh2[threadIdx.x][0] = a;
+  sh2[threadIdx.x] = a;
   __syncthreads();
-#pragma unroll
-  for (int q = 0; q < NS; ++q) {
-    double r = red_identity(ops[q]);
-    for (int kk = 0; kk < L; ++kk) r = red_combine(ops[q], r, sh2[kk * NS + q][0]);
-    out[q] = r;
+  if (threadIdx.x < nslots) {
+    double r = red_identity(ops[threadIdx.x]);
+    for (int kk = 0; kk < L; ++kk) r = red_combine(ops[threadIdx.x], r, sh2[kk * nslots + threadIdx.x]);
+    res[threadIdx.x] = r;
   }
   if (threadIdx.x == 0) *counter = 0u;    // ready for the next kernel on this stream
   __syncthreads();
@@ -219,6 +233,54 @@ __device__ __forceinline__ void stream_rows3(const double* A, const double* B, c
     if (threadIdx.x == 0 && k + MWU_SST < mine) issue(k + MWU_SST, slot);
     ++it;
   }
+}
+
+// ---------------------------------------------------------------- L2 eviction-priority hints
+// Streams (read or written once per sweep) are marked evict_first, so the small vertex vectors
+// that are gathered / scattered at random (u, d^(y): tens of MB) keep their L2 lines (evict_last).
+__device__ __forceinline__ uint64_t pol_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double ldh(const double* a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ldh_nc(const double* a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int ldh_nc(const int* a, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint32_t ldh_nc(const uint32_t* a, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double2 ldh2(const double2* a, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void sth(double* a, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void sth2(double2* a, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(a), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void redh_add(double* a, double v, uint64_t pol) {
+  asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
 }
 
 // Direction d_i = sigma * max{0, 1 - g_i/h_i} * x_i (P:279 / P:666); h_i = 0 -> 0 (Q5).

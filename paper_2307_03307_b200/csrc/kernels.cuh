@@ -15,6 +15,7 @@
 // power-law degree distributions load-balance and results stay deterministic.
 #pragma once
 #include "common.cuh"
+#include "fastmath.cuh"
 
 namespace mwu {
 
@@ -73,9 +74,8 @@ __device__ void stage_double_exps(Ctl* c, const int* ks, int n) {
 // it in few passes (galloping up, then splitting the unknown gap).
 __device__ void stage_double_next(Ctl* c) {
   int ks[MWU_MAXC], n = 0;
-  if (c->dk_hi >= (1 << 20)) {                       // no stop seen yet: gallop upward
-    const int offs[4] = {1, 2, 4, 8};
-    for (int i = 0; i < MWU_MAXC && i < 4; ++i) ks[n++] = c->dk_lo + offs[i];
+  if (c->dk_hi >= (1 << 20)) {                       // no stop seen yet: the next MAXC exponents
+    for (int i = 0; i < MWU_MAXC; ++i) ks[n++] = c->dk_lo + 1 + i;
   } else {                                           // unknown exponents dk_lo+1 .. dk_hi-1
     const int lo = c->dk_lo + 1, hi = c->dk_hi - 1, cnt = hi - lo + 1;
     if (cnt <= MWU_MAXC) {
@@ -98,7 +98,8 @@ __device__ void stage_double_first(Ctl* c) {
   c->dk_hi = 1 << 20;
   int kg = 1;
   if (c->t > 0 && c->alpha_prev >= 1.0) kg = ilogb(c->alpha_prev);
-  int k0 = kg - 1 < 0 ? 0 : kg - 1;
+  int k0 = kg - (MWU_MAXC / 2 - 1);
+  if (k0 < 0) k0 = 0;
   int ks[MWU_MAXC];
   for (int j = 0; j < MWU_MAXC; ++j) ks[j] = k0 + j;
   stage_double_exps(c, ks, MWU_MAXC);
@@ -163,19 +164,39 @@ __device__ __forceinline__ double cand_mn(const Ctl* c, int j, const double* res
   return c->cSing ? (c->zS + c->cand[j] * c->dzS) : res[R_MN(j)];
 }
 
-__device__ void accept_alpha(Ctl* c, double a, double mx, double mn) {
+__device__ __forceinline__ double cand_tc(const Ctl* c, int j, const double* res) { return res[R_TC(j)]; }
+__device__ __forceinline__ double cand_sh(const Ctl* c, int j) { return c->shC[j]; }
+
+__device__ void accept_alpha(Ctl* c, double a, double mx, double mn, double tc, double tsh) {
   c->alpha = a;
   c->newsP = mx;
   c->newsC = mn;
+  c->acc_tc = tc;
+  c->acc_sh = tsh;
   c->sphase = SP_DONE;
   c->sactive = 0;
-  if (a < 1.0) { c->status = ST_INFEASIBLE; c->reason = R_ALPHA_LT_1; }
+  if (a < 1.0) { c->status = ST_INFEASIBLE; c->reason = R_ALPHA_LT_1; return; }
+  if (c->lazyC && !(tc > 1e-280 && isfinite(tc))) {
+    // lazyC carries S_C of the next iterate from this sum; it underflowed at the old shift, so
+    // re-evaluate the accepted alpha with the exact min shift (one extra pass, Q16)
+    c->sphase = SP_TCFIX; c->ncand = 1; c->cand[0] = a; c->cea[0] = c->eta * a; c->cexp[0] = 0; c->csq[0] = 0;
+    c->cmP[0] = CM_EXT; c->cmC[0] = CM_LSE; c->shC[0] = mn; c->ptype = PT_LIST; c->sactive = 1;
+  }
 }
 
 // res layout: see R_* above
 __device__ void search_controller(Ctl* c, const double* res) {
   c->passes_total++;
-  if (c->sphase == SP_FIXED) { accept_alpha(c, c->cand[0], cand_mx(c, 0, res), cand_mn(c, 0, res)); return; }
+  if (c->sphase == SP_FIXED) {
+    accept_alpha(c, c->cand[0], cand_mx(c, 0, res), cand_mn(c, 0, res), cand_tc(c, 0, res), cand_sh(c, 0));
+    return;
+  }
+  if (c->sphase == SP_TCFIX) {
+    const double tc = cand_tc(c, 0, res);
+    if (!(tc > 1e-280 && isfinite(tc))) { c->nan_flag = 1; c->status = ST_INFEASIBLE; c->sactive = 0; return; }
+    accept_alpha(c, c->cand[0], c->newsP, c->newsC, tc, cand_sh(c, 0));
+    return;
+  }
   if (c->sphase == SP_DOUBLE) {
     // classify the evaluated exponents (ascending): pass = f >= 1 and min(z + a dz) < 1
     int lse_j = -1;
@@ -187,8 +208,11 @@ __device__ void search_controller(Ctl* c, const double* res) {
       if (nP || nC) { if (lse_j < 0) lse_j = j; continue; }
       const double mxj = cand_mx(c, j, res), mnj = cand_mn(c, j, res);
       const bool ok = phi >= psi;                                  // eq:b4b_conv
-      if (ok && mnj < 1.0) { c->dk_lo = k; c->ok_mx = mxj; c->ok_mn = mnj; }
-      else { c->dk_hi = k; c->hi_exit = ok ? 1 : 0; c->hi_mx = mxj; c->hi_mn = mnj; }
+      if (ok && mnj < 1.0) { c->dk_lo = k; c->ok_mx = mxj; c->ok_mn = mnj; c->ok_tc = cand_tc(c, j, res); c->ok_sh = cand_sh(c, j); }
+      else {
+        c->dk_hi = k; c->hi_exit = ok ? 1 : 0; c->hi_mx = mxj; c->hi_mn = mnj;
+        c->hi_tc = cand_tc(c, j, res); c->hi_sh = cand_sh(c, j);
+      }
     }
     if (lse_j >= 0 && c->cexp[lse_j] > c->dk_lo && c->cexp[lse_j] < c->dk_hi) {
       // Q16: re-evaluate this exponent with the exact max / min shift
@@ -209,17 +233,18 @@ __device__ void search_controller(Ctl* c, const double* res) {
     const int cap_k = c->max_evals - 1;
     if (c->dk_lo >= cap_k || (c->dk_hi == c->dk_lo + 1 && c->dk_hi > cap_k)) {
       c->evals = c->max_evals; c->evals_total += c->max_evals;
-      if (c->dk_lo == cap_k) { accept_alpha(c, ldexp(1.0, cap_k), c->ok_mx, c->ok_mn); return; }
+      if (c->dk_lo == cap_k) { accept_alpha(c, ldexp(1.0, cap_k), c->ok_mx, c->ok_mn, c->ok_tc, c->ok_sh); return; }
       c->sphase = SP_FIXED; c->ncand = 1; c->cand[0] = ldexp(1.0, cap_k); c->ptype = PT_LIST;   // shifts only
-      c->cea[0] = c->eta * c->cand[0]; c->cmP[0] = CM_EXT; c->cmC[0] = CM_EXT; c->sactive = 1;
+      c->cea[0] = c->eta * c->cand[0]; c->cmP[0] = CM_EXT; c->cmC[0] = c->lazyC ? CM_EXPM1 : CM_EXT;
+      c->shC[0] = c->sC; c->sactive = 1;
       return;
     }
     if (c->dk_hi == c->dk_lo + 1) {
       const int ks = c->dk_hi;
       c->evals = ks + 1; c->evals_total += ks + 1;
-      if (c->hi_exit) { accept_alpha(c, ldexp(1.0, ks), c->hi_mx, c->hi_mn); return; }
+      if (c->hi_exit) { accept_alpha(c, ldexp(1.0, ks), c->hi_mx, c->hi_mn, c->hi_tc, c->hi_sh); return; }
       c->sphase = SP_BISECT; c->lb = ldexp(1.0, ks - 1); c->ub = ldexp(1.0, ks);
-      c->lb_mx = c->ok_mx; c->lb_mn = c->ok_mn;
+      c->lb_mx = c->ok_mx; c->lb_mn = c->ok_mn; c->lb_tc = c->ok_tc; c->lb_sh = c->ok_sh;
     } else {
       stage_double_next(c);
       c->sactive = 1;
@@ -231,7 +256,7 @@ __device__ void search_controller(Ctl* c, const double* res) {
     {
       const double thr = c->tol_prose ? c->eps : (1.0 - c->eps);         // Q9
       if (!((c->ub - c->lb) > thr * c->lb && c->evals < c->max_evals)) {
-        accept_alpha(c, c->lb, c->lb_mx, c->lb_mn);                         // return lb
+        accept_alpha(c, c->lb, c->lb_mx, c->lb_mn, c->lb_tc, c->lb_sh);     // return lb
         return;
       }
       need = (c->lb + c->ub) / 2.0;
@@ -260,7 +285,8 @@ __device__ void search_controller(Ctl* c, const double* res) {
     const bool ok = phi >= psi;                                             // eq:b4b_conv
     c->evals++;
     c->evals_total++;
-    if (ok) { c->lb = need; c->lb_mx = mxj; c->lb_mn = mnj; } else { c->ub = need; }
+    if (ok) { c->lb = need; c->lb_mx = mxj; c->lb_mn = mnj; c->lb_tc = cand_tc(c, j, res); c->lb_sh = cand_sh(c, j); }
+    else { c->ub = need; }
   }
   c->status = ST_INFEASIBLE; c->reason = R_ALPHA_LT_1; c->sactive = 0;   // unreachable guard
 }
@@ -268,8 +294,21 @@ __device__ void search_controller(Ctl* c, const double* res) {
 // =====================================================================================
 // Finalize: control logic run by thread 0 of the last block of a phase kernel
 // =====================================================================================
-__device__ void finalize(Ctl* c, int action, const double* r) {
+__device__ void finalize(Ctl* c, int action, double* r) {
   switch (action) {
+    case A_COL_FAST: {                             // fast densest column: max d, inactive aggregate
+      c->apply_prev = 0;
+      c->maxd = r[0];
+      c->mzi = r[1];
+      // r[2] = sum of v = exp(-eta(z - s_C)) over inactive rows; rescaled to shift mzi.  Exact
+      // unless eta(mzi - s_C) > 600, where terms may have underflowed: inactive_exact redoes it.
+      c->vi_exact = 0;
+      if (!(r[2] > 0.0)) c->Vi = 0.0;
+      else if (c->eta * (c->mzi - c->sC) <= 600.0) c->Vi = r[2] * exp(c->eta * (c->mzi - c->sC));
+      else c->vi_exact = 1;
+      if (!(r[0] > 0.0)) { c->status = ST_INFEASIBLE; c->reason = R_MAXD_ZERO; }
+      break;
+    }
     case A_COL: {
       c->apply_prev = 0;
       c->maxd = r[0];
@@ -287,7 +326,8 @@ __device__ void finalize(Ctl* c, int action, const double* r) {
       c->evals = 0;
       if (c->fixed_alpha > 0.0) {
         c->sphase = SP_FIXED; c->ncand = 1; c->cand[0] = c->fixed_alpha; c->ptype = PT_LIST;
-        c->cea[0] = c->eta * c->fixed_alpha; c->cmP[0] = CM_EXT; c->cmC[0] = CM_EXT;
+        c->cea[0] = c->eta * c->fixed_alpha; c->cmP[0] = CM_EXT; c->cmC[0] = c->lazyC ? CM_EXPM1 : CM_EXT;
+        c->shC[0] = c->sC;
       } else {
         c->sphase = SP_DOUBLE; c->sa = 1.0;                                 // alpha <- 1
         stage_double_first(c);
@@ -297,6 +337,14 @@ __device__ void finalize(Ctl* c, int action, const double* r) {
       break;
     }
     case A_SEARCH:
+      if (c->lazyC) {
+        // covering rows with d^(z) = 0 were not streamed: they add exp(-eta(z - shC)) to the
+        // shifted sums and z to the minima, for every candidate alike
+        for (int j = 0; j < c->ncand; ++j) {
+          r[R_MN(j)] = fmin(r[R_MN(j)], c->mzi);
+          if (c->Vi > 0.0 && c->cmC[j] != CM_EXT) r[R_TC(j)] += c->Vi * exp(-c->eta * (c->mzi - c->shC[j]));
+        }
+      }
       search_controller(c, r);
       set_cond(c->h_search, c->sactive ? 1u : 0u);
       break;
@@ -306,6 +354,7 @@ __device__ void finalize(Ctl* c, int action, const double* r) {
       if (c->pSing) { c->yS = c->yS + c->alpha * c->dyS; c->sP = c->yS; c->SP = 1.0; }
       else { c->sP = c->newsP; c->SP = r[0]; }
       if (c->cSing) { c->zS = c->zS + c->alpha * c->dzS; c->sC = c->zS; c->SC = 1.0; }
+      else if (c->lazyC) { c->sC = c->newsC; c->SC = c->acc_tc * exp(c->eta * (c->newsC - c->acc_sh)); }
       else { c->sC = c->newsC; c->SC = r[1]; }
       if (!(isfinite(c->SP) && isfinite(c->SC) && c->SP > 0.0 && c->SC > 0.0)) {
         c->nan_flag = 1; c->status = ST_INFEASIBLE;
@@ -337,6 +386,10 @@ __device__ void finalize(Ctl* c, int action, const double* r) {
     case A_SUM:
       for (int s = 0; s < MWU_SLOTS; ++s) c->scratch[s] = r[s];
       break;
+    case A_VI_EXACT:
+      c->Vi = r[0];
+      c->vi_exact = 0;
+      break;
     default:
       break;
   }
@@ -346,14 +399,10 @@ __device__ void finalize(Ctl* c, int action, const double* r) {
 template <int NS>
 __device__ __forceinline__ void reduce_and_finalize(double (&acc)[NS], const int* ops, double* part,
                                                     unsigned int* counter, Ctl* c, int action) {
+  __shared__ double res[MWU_SLOTS];
   block_partials<NS>(acc, ops, part);
-  double out[NS];
-  if (last_block_reduce<NS>(ops, part, counter, out)) {
-    if (threadIdx.x == 0) {
-      double r[MWU_SLOTS];
-      for (int s = 0; s < MWU_SLOTS; ++s) r[s] = (s < NS) ? out[s] : 0.0;
-      finalize(c, action, r);
-    }
+  if (last_block_combine(ops, NS, part, counter, res)) {
+    if (threadIdx.x == 0) finalize(c, action, res);
   }
 }
 
@@ -676,35 +725,314 @@ __global__ void __launch_bounds__(MWU_NT) pair_sum(int64_t E, const double* __re
 // =====================================================================================
 constexpr size_t kSearchSmem = (size_t)MWU_SST * 3 * MWU_SCH * sizeof(double);
 
-// One HBM pass evaluating the staged candidates (P:716-727 on cached vectors).
-__global__ void __launch_bounds__(MWU_NT) search_pass(int64_t mP, const double* __restrict__ y,
-                                                      const double* __restrict__ dy, const double* __restrict__ u,
-                                                      int64_t mC, const double* __restrict__ z,
-                                                      const double* __restrict__ dz, const double* __restrict__ v,
-                                                      Ctl* c, double* part, unsigned int* counter) {
+__device__ __forceinline__ int search_slot_op(int s) {
+  const int g = s / MWU_MAXC;            // 0 EP, 1 LP, 2 MX, 3 EC, 4 TC, 5 MN
+  return g == 2 ? OP_MAX : (g == 5 ? OP_MIN : OP_SUM);
+}
+
+// (expm1(x), exp(x)) for x <= 0 with both accurate relative to themselves: expm1 while
+// x >= -ln 2 (then exp = 1 + expm1 >= 1/2), exp below (then expm1 = exp - 1 <= -1/2).
+__device__ __forceinline__ void expm1_exp(double x, double& em, double& q) {
+  if (x >= -0.6931471805599453) { em = expm1(x); q = 1.0 + em; }
+  else { q = exp(x); em = q - 1.0; }
+}
+
+// Candidate parameters of a pass, in registers (uniform over the grid).
+struct Cands {
+  double a[MWU_MAXC], ea[MWU_MAXC], shP[MWU_MAXC], shC[MWU_MAXC];
+  int mP[MWU_MAXC], mC[MWU_MAXC], sq[MWU_MAXC];
+  int nc, pt;
+  double ea0, ead;
+};
+
+// Fast per-row bodies: every candidate of the pass uses the expm1 form (Q16) on the streamed
+// side; the candidates follow from ONE transcendental per row by exact identities
+//   doubling  a -> 2a   : expm1(2x) = e (e + 2),            exp(2x) = q^2
+//   grid  a -> a + delta: expm1(x + w) = e + e_w + e e_w,  exp(x + w) = q q_w
+template <int PT, int NC, bool SQ1>
+struct PRowFast {
+  double a[NC], ea0, ead, eta;
+  int sq[NC];
+  double ep[NC], mx[NC];
+  double shP[NC];
+  bool lse[NC];        // Q16: candidates with eta alpha max d^(y) > 700 use the shifted exp sum
+  __device__ PRowFast(const Cands& k, double e) : ea0(k.ea0), ead(k.ead), eta(e) {
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      a[j] = k.a[j]; sq[j] = k.sq[j]; ep[j] = 0.0; mx[j] = -INFINITY; shP[j] = k.shP[j]; lse[j] = (k.mP[j] == CM_LSE);
+    }
+  }
+  __device__ __forceinline__ void operator()(double y, double d, double u, int64_t = 0) {
+    double em = mwu_expm1(ea0 * d), emd = 0.0;
+    if (PT == PT_GRID) emd = mwu_expm1(ead * d);
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      if (PT == PT_DOUBLE) {
+        if (SQ1) { if (j > 0) em = em * (em + 2.0); }          // consecutive exponents
+        else { for (int s = 0; s < sq[j]; ++s) em = em * (em + 2.0); }
+      } else em = em + emd + em * emd;
+      if (lse[j]) ep[j] += mwu_exp(eta * ((y + a[j] * d) - shP[j]));   // packing side is short
+      else ep[j] = __fma_rn(u, em, ep[j]);
+    }
+    // candidates ascend, so y + a_j d <= y + a_last d: a row can raise a maximum only if that
+    // exceeds the smallest running max (warp-uniform branch)
+    const bool upd = (y + a[NC - 1] * d) > mx[0];
+    if (__any_sync(__activemask(), upd)) {
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        const double t = y + a[j] * d;
+        if (upd && t > mx[j]) mx[j] = t;
+      }
+    }
+  }
+};
+
+template <int PT, int NC, bool SQ1>
+struct CRowFast {
+  double a[NC], ea0, ead;
+  int sq[NC];
+  double ec[NC], tc[NC], mn[NC];
+  __device__ CRowFast(const Cands& k) : ea0(k.ea0), ead(k.ead) {
+#pragma unroll
+    for (int j = 0; j < NC; ++j) { a[j] = k.a[j]; sq[j] = k.sq[j]; ec[j] = 0.0; tc[j] = 0.0; mn[j] = INFINITY; }
+  }
+  __device__ __forceinline__ void operator()(double z, double d, double v, int64_t = 0) {
+    double em, q, emd = 0.0, qd = 1.0;
+    mwu_expm1_exp(-(ea0 * d), em, q);
+    if (PT == PT_GRID) mwu_expm1_exp(-(ead * d), emd, qd);
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      if (PT == PT_DOUBLE) {
+        if (SQ1) { if (j > 0) { em = em * (em + 2.0); q = q * q; } }
+        else { for (int s = 0; s < sq[j]; ++s) { em = em * (em + 2.0); q = q * q; } }
+      } else { em = em + emd + em * emd; q = q * qd; }
+      ec[j] = __fma_rn(v, em, ec[j]);
+      tc[j] = __fma_rn(v, q, tc[j]);
+    }
+    // z + a_j d >= z and the running minima ascend in j: a row can lower a minimum only if
+    // z < mn[NC-1] (rare once the minima settle; warp-uniform branch)
+    const bool upd = z < mn[NC - 1];
+    if (__any_sync(__activemask(), upd)) {
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        const double t = z + a[j] * d;
+        if (upd && t < mn[j]) mn[j] = t;
+      }
+    }
+  }
+  // two rows with their dependent chains interleaved (FP64 latency is the limiter); row 1 is
+  // masked by w1 = 0 (weight 0, z = +inf) when absent
+  __device__ __forceinline__ void pair(double z0, double d0, double v0, double z1, double d1, double v1) {
+    double e0, q0, e1, q1, ed0 = 0.0, qd0 = 1.0, ed1 = 0.0, qd1 = 1.0;
+    mwu_expm1_exp(-(ea0 * d0), e0, q0);
+    mwu_expm1_exp(-(ea0 * d1), e1, q1);
+    if (PT == PT_GRID) { mwu_expm1_exp(-(ead * d0), ed0, qd0); mwu_expm1_exp(-(ead * d1), ed1, qd1); }
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      if (PT == PT_DOUBLE) {
+        if (SQ1) {
+          if (j > 0) { e0 = e0 * (e0 + 2.0); q0 = q0 * q0; e1 = e1 * (e1 + 2.0); q1 = q1 * q1; }
+        } else {
+          for (int s = 0; s < sq[j]; ++s) { e0 = e0 * (e0 + 2.0); q0 = q0 * q0; e1 = e1 * (e1 + 2.0); q1 = q1 * q1; }
+        }
+      } else {
+        e0 = e0 + ed0 + e0 * ed0; q0 = q0 * qd0;
+        e1 = e1 + ed1 + e1 * ed1; q1 = q1 * qd1;
+      }
+      ec[j] = __fma_rn(v1, e1, __fma_rn(v0, e0, ec[j]));
+      tc[j] = __fma_rn(v1, q1, __fma_rn(v0, q0, tc[j]));
+    }
+    const bool u0 = z0 < mn[NC - 1], u1 = z1 < mn[NC - 1];
+    if (__any_sync(__activemask(), u0 || u1)) {
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        const double t0 = z0 + a[j] * d0, t1 = z1 + a[j] * d1;
+        if (u0 && t0 < mn[j]) mn[j] = t0;
+        if (u1 && t1 < mn[j]) mn[j] = t1;
+      }
+    }
+  }
+};
+
+// Generic per-row bodies (any candidate list and modes: fixed steps, exact-shift re-passes).
+struct PRowGen {
+  const Cands& k;
+  double eta;
+  double ep[MWU_MAXC], lp[MWU_MAXC], mx[MWU_MAXC];
+  __device__ PRowGen(const Cands& kk, double e) : k(kk), eta(e) {
+#pragma unroll
+    for (int j = 0; j < MWU_MAXC; ++j) { ep[j] = 0.0; lp[j] = 0.0; mx[j] = -INFINITY; }
+  }
+  __device__ __forceinline__ void operator()(double y, double d, double u, int64_t = 0) {
+#pragma unroll
+    for (int j = 0; j < MWU_MAXC; ++j) {
+      if (j < k.nc) {
+        const double t = y + k.a[j] * d;
+        mx[j] = fmax(mx[j], t);
+        if (k.mP[j] == CM_EXPM1) ep[j] = __fma_rn(u, expm1(k.ea[j] * d), ep[j]);
+        else if (k.mP[j] == CM_LSE) lp[j] += exp(eta * (t - k.shP[j]));
+      }
+    }
+  }
+};
+
+struct CRowGen {
+  __device__ __forceinline__ void pair(double z0, double d0, double v0, double z1, double d1, double v1) {
+    (*this)(z0, d0, v0);
+    if (v1 != 0.0 || z1 != INFINITY) (*this)(z1, d1, v1);
+  }
+  const Cands& k;
+  double neta;
+  double ec[MWU_MAXC], tc[MWU_MAXC], mn[MWU_MAXC];
+  __device__ CRowGen(const Cands& kk, double ne) : k(kk), neta(ne) {
+#pragma unroll
+    for (int j = 0; j < MWU_MAXC; ++j) { ec[j] = 0.0; tc[j] = 0.0; mn[j] = INFINITY; }
+  }
+  __device__ __forceinline__ void operator()(double z, double d, double v, int64_t = 0) {
+#pragma unroll
+    for (int j = 0; j < MWU_MAXC; ++j) {
+      if (j < k.nc) {
+        const double t = z + k.a[j] * d;
+        mn[j] = fmin(mn[j], t);
+        if (k.mC[j] == CM_EXPM1) {
+          double em, q;
+          expm1_exp(-(k.ea[j] * d), em, q);
+          ec[j] = __fma_rn(v, em, ec[j]);
+          tc[j] = __fma_rn(v, q, tc[j]);
+        } else if (k.mC[j] == CM_LSE) {
+          tc[j] += exp(neta * (t - k.shC[j]));
+        }
+      }
+    }
+  }
+};
+
+// Compacted covering rows (fast densest path): warp per tile; the tile's records sit in
+// MWU_NT/32 per-warp segments of kWarpSeg slots with counts tcnt[tile*8 + w]; lanes walk the
+// concatenation (4 rows per lane in flight), so every lane has work whatever the segment sizes.
+template <class F>
+__device__ __forceinline__ void for_compact_rows(const double* __restrict__ rz, const double* __restrict__ rdz,
+                                                 const double* __restrict__ rv, const int32_t* __restrict__ tcnt,
+                                                 int64_t ntiles, F& f) {
+  constexpr int NW = MWU_NT / 32;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * MWU_NT + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * MWU_NT) >> 5;
+  for (int64_t tile = gw; tile < ntiles; tile += nw) {
+    int cw = lane < NW ? __ldg(tcnt + tile * NW + lane) : 0;
+    int pre = cw;                                   // inclusive prefix over the NW segments
+#pragma unroll
+    for (int o = 1; o < NW; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, pre, o);
+      if (lane >= o) pre += t;
+    }
+    int P[NW + 1];                                  // exclusive prefixes, uniform over the warp
+    P[0] = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) P[w + 1] = __shfl_sync(0xffffffffu, pre, w);
+    const int cnt = P[NW];
+    const int64_t base = tile * MWU_CT;
+    for (int r0 = 0; r0 < cnt; r0 += 128) {
+      double zz[4], dd[4], vv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = r0 + q * 32 + lane;
+        if (r < cnt) {
+          int seg = 0, off = 0;
+#pragma unroll
+          for (int w = 1; w < NW; ++w) if (r >= P[w]) { seg = w; off = P[w]; }
+          const int64_t a = base + seg * kWarpSeg + (r - off);
+          zz[q] = __ldcs(rz + a); dd[q] = __ldcs(rdz + a); vv[q] = __ldcs(rv + a);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; q += 2) {
+        const bool ok0 = r0 + q * 32 + lane < cnt, ok1 = r0 + (q + 1) * 32 + lane < cnt;
+        if (ok0) f.pair(zz[q], dd[q], vv[q], ok1 ? zz[q + 1] : INFINITY, ok1 ? dd[q + 1] : 0.0, ok1 ? vv[q + 1] : 0.0);
+      }
+    }
+  }
+}
+
+struct SearchArgs {
+  int64_t mP; const double *y, *dy, *u;
+  int64_t mC; const double *z, *dz, *v;                  // dense covering rows (v: weights)
+  const double *rz, *rdz, *rv; const int32_t* tcnt; int64_t ntiles;   // compacted (rz != nullptr)
+};
+
+template <int PT, int NC, bool SQ1>
+__device__ __forceinline__ void search_body_fast(const SearchArgs& A, const Cands& K, const Ctl* c, double* sbuf,
+                                                 uint64_t* bars, double* part) {
+  uint32_t it = 0;
+  const int opsS[NC] = {};   // all OP_SUM (0)
+  int opsX[NC], opsN[NC];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) { opsX[j] = OP_MAX; opsN[j] = OP_MIN; }
+  {
+    PRowFast<PT, NC, SQ1> f(K, c->eta);
+    if (!c->pSing) stream_rows3(A.y, A.dy, A.u, A.mP, sbuf, bars, it, f);
+    block_partials<NC>(f.ep, opsS, part, R_EP(0));
+    block_partials<NC>(f.ep, opsS, part, R_LP(0));          // LSE-mode candidates read this slot
+    block_partials<NC>(f.mx, opsX, part, R_MX(0));
+  }
+  {
+    CRowFast<PT, NC, SQ1> f(K);
+    if (!c->cSing) {
+      if (A.rz) for_compact_rows(A.rz, A.rdz, A.rv, A.tcnt, A.ntiles, f);
+      else stream_rows3(A.z, A.dz, A.v, A.mC, sbuf, bars, it, f);
+    }
+    block_partials<NC>(f.ec, opsS, part, R_EC(0));
+    block_partials<NC>(f.tc, opsS, part, R_TC(0));
+    block_partials<NC>(f.mn, opsN, part, R_MN(0));
+  }
+}
+
+__device__ __forceinline__ void search_body_gen(const SearchArgs& A, const Cands& K, const Ctl* c, double* sbuf,
+                                                uint64_t* bars, double* part) {
+  uint32_t it = 0;
+  int opsS[MWU_MAXC], opsX[MWU_MAXC], opsN[MWU_MAXC];
+#pragma unroll
+  for (int j = 0; j < MWU_MAXC; ++j) { opsS[j] = OP_SUM; opsX[j] = OP_MAX; opsN[j] = OP_MIN; }
+  {
+    PRowGen f(K, c->eta);
+    if (!c->pSing) stream_rows3(A.y, A.dy, A.u, A.mP, sbuf, bars, it, f);
+    block_partials<MWU_MAXC>(f.ep, opsS, part, R_EP(0));
+    block_partials<MWU_MAXC>(f.lp, opsS, part, R_LP(0));
+    block_partials<MWU_MAXC>(f.mx, opsX, part, R_MX(0));
+  }
+  {
+    CRowGen f(K, -c->eta);
+    if (!c->cSing) {
+      if (A.rz) for_compact_rows(A.rz, A.rdz, A.rv, A.tcnt, A.ntiles, f);
+      else stream_rows3(A.z, A.dz, A.v, A.mC, sbuf, bars, it, f);
+    }
+    block_partials<MWU_MAXC>(f.ec, opsS, part, R_EC(0));
+    block_partials<MWU_MAXC>(f.tc, opsS, part, R_TC(0));
+    block_partials<MWU_MAXC>(f.mn, opsN, part, R_MN(0));
+  }
+}
+
+// One HBM pass evaluating the staged candidates (P:716-727 on cached vectors); the
+// last block replays Alg. 3 (search_controller).
+__global__ void __launch_bounds__(MWU_NT, 2) search_pass(SearchArgs A, Ctl* c, double* part, unsigned int* counter) {
   if (c->status != ST_RUNNING || !c->sactive) {
     if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(c->h_search, 0u);
     return;
   }
-  __shared__ double s_a[MWU_MAXC], s_ea[MWU_MAXC], s_shP[MWU_MAXC], s_shC[MWU_MAXC];
-  __shared__ int s_mP[MWU_MAXC], s_mC[MWU_MAXC], s_sq[MWU_MAXC];
-  if (threadIdx.x < MWU_MAXC) {
-    const int j = threadIdx.x;
-    s_a[j] = c->cand[j]; s_ea[j] = c->cea[j]; s_shP[j] = c->shP[j]; s_shC[j] = c->shC[j];
-    s_mP[j] = c->cmP[j]; s_mC[j] = c->cmC[j]; s_sq[j] = c->csq[j];
-  }
-  __syncthreads();
-  const int nc = c->ncand, pt = c->ptype;
-  const double eta = c->eta, neta = -c->eta;
-  // one transcendental per row and pass (per side): candidates follow by exact identities
-  //   doubling  a -> 2a : expm1(2x) = e (e + 2),           exp(2x) = q^2
-  //   grid  a -> a + delta: expm1(x + w) = e + e_w + e e_w, exp(x + w) = q q_w
-  const double ea0 = eta * c->pa0, ead = eta * c->pdelta;
-  double acc[6 * MWU_MAXC];
+  Cands K;
+  K.nc = c->ncand; K.pt = c->ptype;
+  K.ea0 = c->eta * c->pa0; K.ead = c->eta * c->pdelta;
+  bool fast = (K.pt == PT_DOUBLE || K.pt == PT_GRID);
+  bool sq1 = true;
 #pragma unroll
   for (int j = 0; j < MWU_MAXC; ++j) {
-    acc[R_EP(j)] = 0.0; acc[R_LP(j)] = 0.0; acc[R_MX(j)] = -INFINITY;
-    acc[R_EC(j)] = 0.0; acc[R_TC(j)] = 0.0; acc[R_MN(j)] = INFINITY;
+    K.a[j] = c->cand[j]; K.ea[j] = c->cea[j]; K.shP[j] = c->shP[j]; K.shC[j] = c->shC[j];
+    K.mP[j] = c->cmP[j]; K.mC[j] = c->cmC[j]; K.sq[j] = c->csq[j];
+    if (j < K.nc) {
+      if (j > 0 && K.sq[j] != 1) sq1 = false;
+      if (!(c->pSing || K.mP[j] == CM_EXPM1 || K.mP[j] == CM_LSE)) fast = false;
+      if (!(c->cSing || K.mC[j] == CM_EXPM1)) fast = false;
+    }
   }
   extern __shared__ __align__(128) double sbuf[];
   __shared__ __align__(8) uint64_t bars[MWU_SST];
@@ -713,57 +1041,28 @@ __global__ void __launch_bounds__(MWU_NT) search_pass(int64_t mP, const double* 
     fence_barrier_init();
   }
   __syncthreads();
-  uint32_t it = 0;
-  stream_rows3(y, dy, u, mP, sbuf, bars, it, [&](double yi, double di, double ui, int64_t) {
-    double em = 0.0, emd = 0.0;
-    if (pt != PT_LIST) em = expm1(ea0 * di);
-    if (pt == PT_GRID) emd = expm1(ead * di);
-#pragma unroll
-    for (int j = 0; j < MWU_MAXC; ++j) {
-      if (j < nc) {
-        if (pt == PT_DOUBLE) { for (int s = 0; s < s_sq[j]; ++s) em = em * (em + 2.0); }
-        else if (pt == PT_GRID) em = em + emd + em * emd;
-        else if (s_mP[j] == CM_EXPM1) em = expm1(s_ea[j] * di);
-        const double t = yi + s_a[j] * di;
-        acc[R_MX(j)] = fmax(acc[R_MX(j)], t);
-        if (s_mP[j] == CM_EXPM1) acc[R_EP(j)] = __fma_rn(ui, em, acc[R_EP(j)]);   // sums: any order
-        else if (s_mP[j] == CM_LSE) acc[R_LP(j)] += exp(eta * (t - s_shP[j]));
-      }
-    }
-  });
-  stream_rows3(z, dz, v, mC, sbuf, bars, it, [&](double zi, double di, double vi, int64_t) {
-    double em = 0.0, q = 1.0, emd = 0.0, qd = 1.0;
-    if (pt != PT_LIST) {
-      const double xa = -(ea0 * di);
-      if (xa >= -0.6931471805599453) { em = expm1(xa); q = 1.0 + em; } else { q = exp(xa); em = q - 1.0; }
-      if (pt == PT_GRID) {
-        const double xd = -(ead * di);
-        if (xd >= -0.6931471805599453) { emd = expm1(xd); qd = 1.0 + emd; } else { qd = exp(xd); emd = qd - 1.0; }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < MWU_MAXC; ++j) {
-      if (j < nc) {
-        if (pt == PT_DOUBLE) { for (int s = 0; s < s_sq[j]; ++s) { em = em * (em + 2.0); q = q * q; } }
-        else if (pt == PT_GRID) { em = em + emd + em * emd; q = q * qd; }
-        else if (s_mC[j] == CM_EXPM1) {
-          const double xa = -(s_ea[j] * di);
-          if (xa >= -0.6931471805599453) { em = expm1(xa); q = 1.0 + em; } else { q = exp(xa); em = q - 1.0; }
-        }
-        const double t = zi + s_a[j] * di;
-        acc[R_MN(j)] = fmin(acc[R_MN(j)], t);
-        if (s_mC[j] == CM_EXPM1) { acc[R_EC(j)] = __fma_rn(vi, em, acc[R_EC(j)]); acc[R_TC(j)] = __fma_rn(vi, q, acc[R_TC(j)]); }
-        else if (s_mC[j] == CM_LSE) acc[R_TC(j)] += exp(neta * (t - s_shC[j]));
-      }
-    }
-  });
-  int ops[6 * MWU_MAXC];
-#pragma unroll
-  for (int j = 0; j < MWU_MAXC; ++j) {
-    ops[R_EP(j)] = OP_SUM; ops[R_LP(j)] = OP_SUM; ops[R_MX(j)] = OP_MAX;
-    ops[R_EC(j)] = OP_SUM; ops[R_TC(j)] = OP_SUM; ops[R_MN(j)] = OP_MIN;
+  if (fast) {
+#define MWU_FAST_CASE(PTV, N, S) \
+    if (K.pt == PTV && K.nc == N && sq1 == S) search_body_fast<PTV, N, S>(A, K, c, sbuf, bars, part); else
+    MWU_FAST_CASE(PT_DOUBLE, 8, true) MWU_FAST_CASE(PT_DOUBLE, 7, true) MWU_FAST_CASE(PT_DOUBLE, 6, true)
+    MWU_FAST_CASE(PT_DOUBLE, 5, true) MWU_FAST_CASE(PT_DOUBLE, 4, true) MWU_FAST_CASE(PT_DOUBLE, 3, true)
+    MWU_FAST_CASE(PT_DOUBLE, 2, true) MWU_FAST_CASE(PT_DOUBLE, 1, true)
+    MWU_FAST_CASE(PT_DOUBLE, 8, false) MWU_FAST_CASE(PT_DOUBLE, 7, false) MWU_FAST_CASE(PT_DOUBLE, 6, false)
+    MWU_FAST_CASE(PT_DOUBLE, 5, false) MWU_FAST_CASE(PT_DOUBLE, 4, false) MWU_FAST_CASE(PT_DOUBLE, 3, false)
+    MWU_FAST_CASE(PT_DOUBLE, 2, false)
+    MWU_FAST_CASE(PT_GRID, 7, true) MWU_FAST_CASE(PT_GRID, 3, true) MWU_FAST_CASE(PT_GRID, 1, true)
+    search_body_gen(A, K, c, sbuf, bars, part);
+#undef MWU_FAST_CASE
+  } else {
+    search_body_gen(A, K, c, sbuf, bars, part);
   }
-  reduce_and_finalize<6 * MWU_MAXC>(acc, ops, part, counter, c, A_SEARCH);
+  __shared__ double res[MWU_SLOTS];
+  int ops[MWU_SLOTS];
+#pragma unroll
+  for (int s = 0; s < MWU_SLOTS; ++s) ops[s] = search_slot_op(s);
+  if (last_block_combine(ops, MWU_SLOTS, part, counter, res)) {
+    if (threadIdx.x == 0) finalize(c, A_SEARCH, res);
+  }
 }
 
 // y += alpha d^(y), z += alpha d^(z) fused with u = exp(eta (y - s_P)),
@@ -786,14 +1085,14 @@ __global__ void __launch_bounds__(MWU_NT) update_rows(int64_t mP, double* __rest
     double yi = y[i];
     if (has_delta) { yi = yi + a * dy[i]; y[i] = yi; }
     const double w = exp(eta * (yi - sP));
-    u[i] = w;
+    if (u) u[i] = w;
     acc[0] += w;
   }
   for (int64_t i = tid; i < mC; i += stride) {
     double zi = z[i];
     if (has_delta) { zi = zi + a * dz[i]; z[i] = zi; }
     const double w = exp(neta * (zi - sC));
-    v[i] = w;
+    if (v) v[i] = w;
     acc[1] += w;
   }
   const int ops[2] = {OP_SUM, OP_SUM};
@@ -855,6 +1154,232 @@ __global__ void __launch_bounds__(MWU_NT) reduce_vec(int64_t n, const double* __
   }
   const int ops[2] = {OP_SUM, OP_MAX};
   reduce_and_finalize<2>(acc, ops, part, counter, c, A_SUM);
+}
+
+
+// =====================================================================================
+// Fast densest path: column kernel fused with the lazy z update, the weights
+// v = exp(-eta (z - s_C)) recomputed from z, the forward product d^(y) = (1/D) O d scattered
+// with fp64 reductions into the (L2-resident) vertex vector, and per-tile compaction of the
+// covering rows with d^(z) > 0 for the search passes.
+// =====================================================================================
+// Warp-segmented sum over lanes holding nondecreasing keys (edges sorted by src): the last lane
+// of each run of equal keys returns the run's sum in `out` (others return false).
+__device__ __forceinline__ bool warp_run_sum(int key, double val, double& out) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double ov = __shfl_up_sync(0xffffffffu, val, o);
+    const int ok = __shfl_up_sync(0xffffffffu, key, o);
+    if (lane >= o && ok == key) val += ov;
+  }
+  const int nk = __shfl_down_sync(0xffffffffu, key, 1);
+  out = val;
+  return lane == 31 || nk != key;
+}
+
+__device__ __forceinline__ void red_add_f64(double* p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+
+// act: bit e = (d_2e, d_2e+1) != 0 in the last computed direction (word e >> 5, bit e & 31).
+// Edges with a clear bit have d = 0 (their d slots in memory are stale and never read), so the
+// kernel reads x and d, and writes x, z and d, only for edges active in this or the last step.
+__device__ __forceinline__ bool act_bit(const uint32_t* act, int e) { return (__ldg(act + (e >> 5)) >> (e & 31)) & 1u; }
+
+// Software-pipelined over tiles: the streamed inputs of tile i+1 (z, src/dst rows, activity
+// word) and its u gathers are in flight while tile i is computed, so the DRAM latency of the
+// stream and the L2 latency of the gathers overlap the (exp / division heavy) arithmetic.
+struct ColIn {
+  double z[kColEdges];
+  int sr[kColEdges], dr[kColEdges];
+  uint32_t pw[kColEdges];
+};
+
+__device__ __forceinline__ void col_load(ColIn& in, int tile, int E, const double* __restrict__ z,
+                                         const int32_t* __restrict__ srow, const int32_t* __restrict__ drow,
+                                         const uint32_t* __restrict__ act) {
+#pragma unroll
+  for (int k = 0; k < kColEdges; ++k) {
+    const int e = tile * MWU_CT + k * MWU_NT + threadIdx.x;
+    if (e < E) {
+      in.pw[k] = __ldg(act + (e >> 5));
+      in.z[k] = __ldcs(z + e);
+      in.sr[k] = __ldcs(srow + e);
+      in.dr[k] = __ldcs(drow + e);
+    } else {
+      in.pw[k] = 0u; in.z[k] = INFINITY; in.sr[k] = -1; in.dr[k] = -1;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(MWU_NT, 3) col_densest_fast(
+    int64_t E64, const int32_t* __restrict__ srow, const int32_t* __restrict__ drow, const double* __restrict__ u,
+    double* __restrict__ x, double* __restrict__ d, double* __restrict__ z, double* __restrict__ dy,
+    uint32_t* __restrict__ act, double* __restrict__ rz, double* __restrict__ rdz, double* __restrict__ rv,
+    int32_t* __restrict__ tcnt, double* gdbg, double* hdbg, Ctl* c, double* part, unsigned int* counter) {
+  if (c->status != ST_RUNNING) return;
+  const double rSP = 1.0 / c->SP, rSC = 1.0 / c->SC, invD = c->invB, sigma = c->sigma, ap = c->alpha_prev;
+  const double neta = -c->eta, sC = c->sC;
+  const int apply = c->apply_prev;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int E = (int)E64;                  // the fast path requires E < 2^31 - MWU_CT (host check)
+  double maxd = -INFINITY;
+  double im = INFINITY, is = 0.0;          // inactive rows: min z and sum of v (shift s_C)
+  double2* x2 = reinterpret_cast<double2*>(x);
+  double2* d2 = reinterpret_cast<double2*>(d);
+  const int ntiles = (E + MWU_CT - 1) / MWU_CT;
+  int tile = blockIdx.x;
+  ColIn cur, nxt;
+  double us[kColEdges], ud[kColEdges];
+  if (tile < ntiles) {
+    col_load(cur, tile, E, z, srow, drow, act);
+#pragma unroll
+    for (int k = 0; k < kColEdges; ++k)
+      if (cur.sr[k] >= 0) { us[k] = __ldg(u + cur.sr[k]); ud[k] = __ldg(u + cur.dr[k]); }
+  }
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int tn = tile + gridDim.x;
+    if (tn < ntiles) col_load(nxt, tn, E, z, srow, drow, act);    // next tile's stream, in flight
+    const int e0 = tile * MWU_CT + threadIdx.x;
+    int nact = 0;
+    double zk[kColEdges], dzk[kColEdges], vk[kColEdges];
+#pragma unroll
+    for (int k = 0; k < kColEdges; ++k) {
+      const int e = e0 + k * MWU_NT;
+      const bool had = (cur.pw[k] >> lane) & 1u;
+      double2 xe = make_double2(0.0, 0.0), dp = xe;
+      if (had) { xe = x2[e]; dp = d2[e]; }
+      double zz = cur.z[k];
+      double d0 = 0.0, d1 = 0.0, v = 0.0;
+      if (e < E) {
+        if (apply && had) {                                       // lazy x, z += alpha d
+          xe.x = xe.x + ap * dp.x;
+          xe.y = xe.y + ap * dp.y;
+          x2[e] = xe;
+          const double dzp = dp.x + dp.y;                         // d^(z)_e = (W d)_e of the last step
+          zz = zz + ap * dzp;
+          z[e] = zz;
+        }
+        v = mwu_exp(neta * (zz - sC));                                // covering weight (Q4)
+        const double h = v * rSC;                                 // W^T w_c
+        const double g0 = invD * (us[k] * rSP);                   // (1/D) O^T w_p
+        const double g1 = invD * (ud[k] * rSP);
+        if (gdbg) { gdbg[2 * e] = g0; gdbg[2 * e + 1] = g1; hdbg[2 * e] = h; hdbg[2 * e + 1] = h; }
+        // g >= h gives fl(g/h) >= 1, i.e. d = 0 exactly
+        const bool a0 = g0 < h, a1 = g1 < h;
+        if ((a0 || a1) && !had) xe = x2[e];                       // newly active: fetch x
+        if (a0) d0 = mwu_direction(g0, h, xe.x, sigma);
+        if (a1) d1 = mwu_direction(g1, h, xe.y, sigma);
+      }
+      const double dz = d0 + d1;
+      const bool nz = dz > 0.0;
+      if (nz) { d2[e] = make_double2(d0, d1); ++nact; const double m01 = d0 > d1 ? d0 : d1; maxd = m01 > maxd ? m01 : maxd; }
+      else if (e < E) { im = zz < im ? zz : im; is += v; maxd = maxd > 0.0 ? maxd : 0.0; }   // candidate-independent row
+      zk[k] = zz; dzk[k] = dz; vk[k] = v;
+      const uint32_t bw = __ballot_sync(0xffffffffu, nz);
+      if (lane == 0 && e < E && bw != cur.pw[k]) act[e >> 5] = bw;
+      if (d1 > 0.0) red_add_f64(dy + cur.dr[k], invD * d1);       // dst side: random rows
+      // src side: edges are sorted by src, so lanes of a warp hold runs of equal rows
+      const double val = d0 > 0.0 ? invD * d0 : 0.0;
+      if (__any_sync(0xffffffffu, val > 0.0)) {
+        double run;
+        if (warp_run_sum(cur.sr[k], val, run) && run > 0.0) red_add_f64(dy + cur.sr[k], run);
+      }
+    }
+    // the next tile's gathers (its src/dst rows have arrived by now)
+    if (tn < ntiles) {
+#pragma unroll
+      for (int k = 0; k < kColEdges; ++k)
+        if (nxt.sr[k] >= 0) { us[k] = __ldg(u + nxt.sr[k]); ud[k] = __ldg(u + nxt.dr[k]); }
+    }
+    // compaction of the active covering rows: each warp owns the record segment
+    // [tile*CT + warp*kWarpSeg, +kWarpSeg) of its kWarpSeg edges (no block barrier)
+    int incl = nact;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    int p = tile * MWU_CT + warp * kWarpSeg + incl - nact;
+#pragma unroll
+    for (int k = 0; k < kColEdges; ++k)
+      if (dzk[k] > 0.0) { rz[p] = zk[k]; rdz[p] = dzk[k]; rv[p] = vk[k]; ++p; }
+    if (lane == 31) tcnt[tile * (MWU_NT / 32) + warp] = incl;
+    cur = nxt;
+  }
+  double acc[3] = {maxd, im, is};
+  const int ops[3] = {OP_MAX, OP_MIN, OP_SUM};
+  reduce_and_finalize<3>(acc, ops, part, counter, c, A_COL_FAST);
+}
+
+// Rare path of the inactive-row aggregate: when min_inactive z - s_C exceeds 600/eta the sum of
+// v at shift s_C may have lost terms to underflow; recompute it at shift mzi exactly.
+__global__ void __launch_bounds__(MWU_NT) inactive_exact(int64_t E, const uint32_t* __restrict__ act,
+                                                         const double* __restrict__ z, Ctl* c, double* part,
+                                                         unsigned int* counter) {
+  if (c->status != ST_RUNNING || !c->vi_exact) return;
+  const double neta = -c->eta, m = c->mzi;
+  double acc[1] = {0.0};
+  for (int64_t e = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; e < E; e += (int64_t)gridDim.x * MWU_NT)
+    if (!act_bit(act, (int)e)) acc[0] += exp(neta * (z[e] - m));
+  const int ops[1] = {OP_SUM};
+  reduce_and_finalize<1>(acc, ops, part, counter, c, A_VI_EXACT);
+}
+
+// max d^(y) over the packing rows once the scattered forward product is complete; sets up the
+// step search (A_STEP_DONE).
+__global__ void __launch_bounds__(MWU_NT) dy_finalize(int64_t mP, const double* __restrict__ dy, Ctl* c, double* part,
+                                                      unsigned int* counter) {
+  if (c->status != ST_RUNNING) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(c->h_search, 0u);
+    return;
+  }
+  double acc[1] = {-INFINITY};
+  for (int64_t i = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; i < mP; i += (int64_t)gridDim.x * MWU_NT)
+    acc[0] = fmax(acc[0], dy[i]);
+  const int ops[1] = {OP_MAX};
+  reduce_and_finalize<1>(acc, ops, part, counter, c, A_STEP_DONE + 100);
+}
+
+// Apply the pending lazy update x += alpha d, z += alpha (W d) (end of probe / vector hooks).
+__global__ void flush_pairs(int64_t E, double* __restrict__ x, const double* __restrict__ d, double* __restrict__ z,
+                            const uint32_t* __restrict__ act, const Ctl* c) {
+  if (!c->apply_prev) return;
+  const double a = c->alpha_prev;
+  double2* x2 = reinterpret_cast<double2*>(x);
+  const double2* d2 = reinterpret_cast<const double2*>(d);
+  for (int64_t e = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; e < E; e += (int64_t)gridDim.x * MWU_NT) {
+    if (act_bit(act, (int)e)) {
+      const double2 dp = d2[e];
+      double2 xe = x2[e];
+      xe.x = xe.x + a * dp.x;
+      xe.y = xe.y + a * dp.y;
+      x2[e] = xe;
+      const double dzp = dp.x + dp.y;
+      z[e] = z[e] + a * dzp;
+    }
+  }
+}
+
+// Vector hooks of the fast densest path: d (zeros where the activity bit is clear) and
+// d^(z)_e = d_2e + d_2e+1 (W d), regardless of the probe status.
+__global__ void d_from_act(int64_t E, const double* __restrict__ d, const uint32_t* __restrict__ act,
+                           double* __restrict__ dout, double* __restrict__ dzout) {
+  const double2* d2 = reinterpret_cast<const double2*>(d);
+  for (int64_t e = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; e < E; e += (int64_t)gridDim.x * MWU_NT) {
+    const double2 a = act_bit(act, (int)e) ? d2[e] : make_double2(0.0, 0.0);
+    if (dout) { dout[2 * e] = a.x; dout[2 * e + 1] = a.y; }
+    if (dzout) dzout[e] = a.x + a.y;
+  }
+}
+
+// w_c = exp(-eta (z - s_C)) / S_C from z (vector hook of the lazy covering side).
+__global__ void wc_from_z(int64_t m, const double* __restrict__ z, double* __restrict__ out, const Ctl* c) {
+  const double neta = -c->eta, sC = c->sC, SC = c->SC;
+  for (int64_t i = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; i < m; i += (int64_t)gridDim.x * MWU_NT)
+    out[i] = exp(neta * (z[i] - sC)) / SC;
 }
 
 }  // namespace mwu

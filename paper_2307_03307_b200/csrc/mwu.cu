@@ -74,6 +74,12 @@ struct mwu_ctx {
   // CSR storage
   Seg csrP, cscP, csrC, cscC;
   double *colmaxP = nullptr, *colsumC = nullptr, *crecipC = nullptr, *crecipP = nullptr;
+  // fast densest path (lazyC): compacted covering-row records per MWU_CT-edge tile
+  int lazyC = 0;
+  int64_t ntilesC = 0;
+  double *rz = nullptr, *rdz = nullptr, *rv = nullptr;
+  int32_t* tcnt = nullptr;
+  uint32_t* act = nullptr;   // activity bits of d (bit e: edge e's pair of directions is nonzero)
   // vectors
   double *x = nullptr, *d = nullptr, *y = nullptr, *dy = nullptr, *u = nullptr, *z = nullptr, *dz = nullptr,
          *v = nullptr, *gtmp = nullptr, *gdbg = nullptr, *hdbg = nullptr, *xbest = nullptr, *tmp = nullptr;
@@ -249,8 +255,18 @@ void alloc_vectors(mwu_ctx* c) {
   c->dy = dalloc<double>(c, c->mP);
   c->u = dalloc<double>(c, c->mP);
   c->z = dalloc<double>(c, c->mC);
-  c->dz = dalloc<double>(c, c->mC);
-  c->v = dalloc<double>(c, c->mC);
+  if (c->lazyC) {
+    c->ntilesC = (c->E + MWU_CT - 1) / MWU_CT;
+    c->rz = dalloc<double>(c, c->ntilesC * MWU_CT);
+    c->rdz = dalloc<double>(c, c->ntilesC * MWU_CT);
+    c->rv = dalloc<double>(c, c->ntilesC * MWU_CT);
+    c->tcnt = dalloc<int32_t>(c, c->ntilesC * (MWU_NT / 32));
+    c->act = dalloc<uint32_t>(c, c->ntilesC * (MWU_CT / 32));
+    CK(cudaMemsetAsync(c->act, 0, c->ntilesC * (MWU_CT / 32) * sizeof(uint32_t), c->st));
+  } else {
+    c->dz = dalloc<double>(c, c->mC);
+    c->v = dalloc<double>(c, c->mC);
+  }
   int64_t mx = c->n;
   if (c->mP > mx) mx = c->mP;
   if (c->mC > mx) mx = c->mC;
@@ -260,7 +276,7 @@ void alloc_vectors(mwu_ctx* c) {
   CK(cudaMemsetAsync(c->x, 0, c->n * sizeof(double), c->st));
   CK(cudaMemsetAsync(c->xbest, 0, c->n * sizeof(double), c->st));
   CK(cudaMemsetAsync(c->dy, 0, (c->mP > 0 ? c->mP : 1) * sizeof(double), c->st));
-  CK(cudaMemsetAsync(c->dz, 0, (c->mC > 0 ? c->mC : 1) * sizeof(double), c->st));
+  if (c->dz) CK(cudaMemsetAsync(c->dz, 0, (c->mC > 0 ? c->mC : 1) * sizeof(double), c->st));
 }
 
 void init_ctx_common(mwu_ctx* c, const mwu_options* opt) {
@@ -507,6 +523,17 @@ void enqueue_column(mwu_ctx* c, cudaStream_t st) {
       c->launches++;
       break;
     case K_DENSEST:
+      if (c->lazyC) {
+        CK(cudaMemsetAsync(c->dy, 0, (c->mP > 0 ? c->mP : 1) * sizeof(double), st));
+        const int64_t nt = c->ntilesC;
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(nt, 3 * c->sms));
+        col_densest_fast<<<g, MWU_NT, 0, st>>>(c->E, c->srow, c->drow, c->u, c->x, c->d, c->z, c->dy, c->act, c->rz,
+                                              c->rdz, c->rv, c->tcnt, c->record ? c->gdbg : nullptr,
+                                              c->record ? c->hdbg : nullptr, c->ctl, c->part, c->counter);
+        inactive_exact<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, c->act, c->z, c->ctl, c->part, c->counter);
+        c->launches += 2;
+        break;
+      }
       col_densest<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, c->srow, c->drow, c->u, c->v, c->x, c->d, c->dz,
                                                         c->record ? c->gdbg : nullptr, c->record ? c->hdbg : nullptr,
                                                         c->ctl, c->part, c->counter);
@@ -544,6 +571,11 @@ void enqueue_forward(mwu_ctx* c, cudaStream_t st, const double* in, double* oy, 
       launch_seg(c, st, c->inc_p, item_of(c->inc_p, in, 1, nullptr), ey, a_done_p);
       break;
     case K_DENSEST:
+      if (!init && c->lazyC) {               // d^(y) was scattered by the column kernel
+        dy_finalize<<<rows_grid(c, c->mP), MWU_NT, 0, st>>>(c->mP, c->dy, c->ctl, c->part, c->counter);
+        c->launches++;
+        break;
+      }
       if (init) {
         pair_sum<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, in, oz, c->ctl);
         c->launches++;
@@ -573,14 +605,20 @@ void enqueue_forward(mwu_ctx* c, cudaStream_t st, const double* in, double* oy, 
 void enqueue_search(mwu_ctx* c, cudaStream_t st) {
   const int64_t chunks = (std::max(c->mP, c->mC) + MWU_SCH - 1) / MWU_SCH;
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>(2 * c->sms, chunks));   // 2 CTAs / SM
-  search_pass<<<g, MWU_NT, kSearchSmem, st>>>(c->mP, c->y, c->dy, c->u, c->mC, c->z, c->dz, c->v,
-                                              c->ctl, c->part, c->counter);
+  SearchArgs A;
+  A.mP = c->mP; A.y = c->y; A.dy = c->dy; A.u = c->u;
+  A.mC = c->mC; A.z = c->z; A.dz = c->dz; A.v = c->v;
+  A.rz = c->rz; A.rdz = c->rdz; A.rv = c->rv; A.tcnt = c->tcnt; A.ntiles = c->ntilesC;
+  search_pass<<<g, MWU_NT, kSearchSmem, st>>>(A, c->ctl, c->part, c->counter);
   c->launches++;
 }
 
 void enqueue_update(mwu_ctx* c, cudaStream_t st, int has_delta) {
-  update_rows<<<rows_grid(c, c->mP + c->mC), MWU_NT, 0, st>>>(c->mP, c->y, c->dy, c->u, c->mC, c->z, c->dz, c->v,
-                                                             c->ctl, c->part, c->counter, has_delta);
+  // lazyC: the covering side is updated lazily by the next column kernel (only at init are its
+  // weight sums formed here, without storing v)
+  const int64_t mC = (c->lazyC && has_delta) ? 0 : c->mC;
+  update_rows<<<rows_grid(c, c->mP + mC), MWU_NT, 0, st>>>(c->mP, c->y, c->dy, c->u, mC, c->z, c->dz, c->v,
+                                                          c->ctl, c->part, c->counter, has_delta);
   c->launches++;
 }
 
@@ -661,6 +699,7 @@ void probe_begin(mwu_ctx* c, double bound, double eps) {
   h.max_evals = c->opt.max_evals;
   h.bisect_depth = c->opt.bisect_depth;
   h.use_graph = c->opt.use_graph;
+  h.lazyC = c->lazyC;
   h.status = c->empty_cover ? ST_INFEASIBLE : ST_RUNNING;
   h.reason = c->empty_cover ? R_EMPTY_COVER : R_NONE;
   h.record = c->record;
@@ -668,6 +707,7 @@ void probe_begin(mwu_ctx* c, double bound, double eps) {
   h.h_iter = 0;     // conditional handles are live only while the probe graph runs
   h.h_search = 0;
   CK(cudaMemcpyAsync(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, c->st));
+  if (c->lazyC) CK(cudaMemsetAsync(c->act, 0, c->ntilesC * (MWU_CT / 32) * sizeof(uint32_t), c->st));
   // x_i = eps / (n ||P_{:,i}||_inf)
   double cm = 1.0;
   const double* colmax = nullptr;
@@ -782,7 +822,8 @@ void profile_iters(mwu_ctx* c, int64_t k, double* out) {
 }
 
 void flush(mwu_ctx* c) {
-  flush_x<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->x, c->d, c->ctl);
+  if (c->lazyC) flush_pairs<<<rows_grid(c, c->E), MWU_NT, 0, c->st>>>(c->E, c->x, c->d, c->z, c->act, c->ctl);
+  else flush_x<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->x, c->d, c->ctl);
   CKL();
   int zero = 0;
   CK(cudaMemcpyAsync(&c->ctl->apply_prev, &zero, sizeof(int), cudaMemcpyHostToDevice, c->st));
@@ -988,6 +1029,7 @@ void mwu_default_options(mwu_options* o) {
   o->world = 1;
   o->rank = 0;
   o->nccl_id = nullptr;
+  o->deterministic = 0;
 }
 
 const char* mwu_last_error(const mwu_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
@@ -1024,6 +1066,7 @@ mwu_status mwu_create_graph(const mwu_graph* g, const mwu_options* opt, mwu_ctx*
       case MWU_G_DENSEST:
         if (g->n_edges == 0) throw MwuError{MWU_ERR_ARG, "densest subgraph needs at least one edge"};
         c->kind = K_DENSEST; c->mode = MWU_MIXED; c->n = 2 * c->E; c->mP = c->nprime; c->mC = c->E;
+        c->lazyC = (c->opt.deterministic || c->E >= (int64_t(1) << 31) - MWU_CT) ? 0 : 1;
         c->nnzP = 2 * c->E; c->nnzC = 2 * c->E; c->empty_dropped = c->nv - c->nprime;
         break;
     }
@@ -1216,20 +1259,43 @@ mwu_status mwu_get_vec(mwu_ctx* c, int which, double* out, int64_t len) {
     bool use_scal = false;
     switch (which) {
       case MWU_VEC_X: flush(c); src = c->x; break;
-      case MWU_VEC_D: src = c->d; break;
+      case MWU_VEC_D:
+        if (c->lazyC) {
+          d_from_act<<<rows_grid(c, c->E), MWU_NT, 0, c->st>>>(c->E, c->d, c->act, c->tmp, nullptr);
+          CKL();
+          src = c->tmp;
+        } else src = c->d;
+        break;
       case MWU_VEC_XBEST: src = c->xbest; break;
       case MWU_VEC_G: src = c->gdbg; break;
       case MWU_VEC_H: src = c->hdbg; break;
       case MWU_VEC_Y: if (c->pSing) { scal = h.yS; use_scal = true; } else src = c->y; break;
       case MWU_VEC_DY: if (c->pSing) { scal = h.dyS; use_scal = true; } else src = c->dy; break;
-      case MWU_VEC_Z: if (c->cSing) { scal = h.zS; use_scal = true; } else src = c->z; break;
-      case MWU_VEC_DZ: if (c->cSing) { scal = h.dzS; use_scal = true; } else src = c->dz; break;
+      case MWU_VEC_Z:
+        if (c->cSing) { scal = h.zS; use_scal = true; }
+        else { if (c->lazyC) flush(c); src = c->z; }
+        break;
+      case MWU_VEC_DZ:
+        if (c->cSing) { scal = h.dzS; use_scal = true; }
+        else if (c->lazyC) {
+          d_from_act<<<rows_grid(c, c->E), MWU_NT, 0, c->st>>>(c->E, c->d, c->act, nullptr, c->tmp);
+          CKL();
+          src = c->tmp;
+        }
+        else src = c->dz;
+        break;
       case MWU_VEC_WP:
         if (c->pSing) { scal = 1.0; use_scal = true; }
         else { scale_div<<<rows_grid(c, c->mP), MWU_NT, 0, c->st>>>(c->mP, c->u, c->tmp, &c->ctl->SP); CKL(); src = c->tmp; }
         break;
       case MWU_VEC_WC:
         if (c->cSing) { scal = 1.0; use_scal = true; }
+        else if (c->lazyC) {
+          flush(c);
+          wc_from_z<<<rows_grid(c, c->mC), MWU_NT, 0, c->st>>>(c->mC, c->z, c->tmp, c->ctl);
+          CKL();
+          src = c->tmp;
+        }
         else { scale_div<<<rows_grid(c, c->mC), MWU_NT, 0, c->st>>>(c->mC, c->v, c->tmp, &c->ctl->SC); CKL(); src = c->tmp; }
         break;
     }

@@ -44,7 +44,7 @@ class Options(ctypes.Structure):
     _fields_ = [("eta_factor", ctypes.c_double), ("max_iter", ctypes.c_int64), ("tol_prose", ctypes.c_int),
                 ("max_evals", ctypes.c_int), ("outer_rel_tol", ctypes.c_double), ("use_graph", ctypes.c_int),
                 ("bisect_depth", ctypes.c_int), ("device", ctypes.c_int), ("world", ctypes.c_int),
-                ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p)]
+                ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p), ("deterministic", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):

@@ -219,13 +219,42 @@ def test_full_solve_csr_mixed(cuda_ok):
 
 # ------------------------------------------------------------------ modes and edge cases
 def test_graph_and_host_modes_bit_identical(cuda_ok):
+    """deterministic=1: every reduction in a fixed order, so the CUDA-graph probe and the
+    host-driven loop agree bit for bit."""
     G = gg.rmat(10, 16, seed=9)
-    a = solver_for("densest", G, use_graph=1)
-    b = solver_for("densest", G, use_graph=0)
+    a = solver_for("densest", G, use_graph=1, deterministic=1)
+    b = solver_for("densest", G, use_graph=0, deterministic=1)
     a.solve(0.1, 300)
     b.solve(0.1, 300)
     assert a.stats()["iters_total"] == b.stats()["iters_total"]
     assert torch.equal(a.x(), b.x())
+
+
+@pytest.mark.parametrize("i", [0, 1])
+def test_densest_deterministic_path_parity(cuda_ok, i):
+    """The fixed-order densest path (deterministic=1: stored v and d^(z), gathered forward
+    product) under the same lockstep checks as the default atomic-scatter path."""
+    G = _graph("densest", i)
+    s, d = G.numpy()
+    B, _ = _oracle_probe_bound("densest", G)
+    lp = O.graph_lp("densest", s, d, G.n_vertices, B)
+    probe = O.Probe(lp, EPS["densest"], max_iter=5000)
+    S = solver_for("densest", G, deterministic=1)
+    lockstep(S, probe, B, EPS["densest"], 50, alphas=None,
+             window=self_sensitivity_window(lp, EPS["densest"], None, 50))
+
+
+def test_densest_fast_path_repeatable_objective(cuda_ok):
+    """The atomic-scatter path varies run to run only in summation order: two solves agree on
+    the outcome, bound and iteration count of a well-separated instance."""
+    G = gg.rmat(10, 16, seed=9)
+    a = solver_for("densest", G)
+    b = solver_for("densest", G)
+    a.solve(0.1, 300)
+    b.solve(0.1, 300)
+    sa, sb = a.stats(), b.stats()
+    assert sa["bound"] == pytest.approx(sb["bound"], rel=1e-6)
+    assert sa["probes"] == sb["probes"]
 
 
 def test_bisect_depth_does_not_change_results(cuda_ok):
