@@ -1314,6 +1314,74 @@ __global__ void __launch_bounds__(MWU_NT, 3) col_densest_fast(
   reduce_and_finalize<3>(acc, ops, part, counter, c, A_COL_FAST);
 }
 
+// Fast MATCH / BMATCH column (P = M, C = (1/M) 1^T): lazy x += alpha d,
+// g_e = w_p[r(src)] + w_p[r(dst)] (M^T), d_e, and the forward product
+// d^(y) = M d scattered into the vertex vector (src side: warp-segmented runs of the sorted edge
+// list; dst side: one fp64 reduction per nonzero d_e).  Reduces max d and sum(d)/M.
+__global__ void __launch_bounds__(MWU_NT, 3) col_match_fast(int64_t E, const int32_t* __restrict__ srow,
+                                                         const int32_t* __restrict__ drow,
+                                                         const double* __restrict__ u, double* __restrict__ x,
+                                                         double* __restrict__ d, double* __restrict__ dy,
+                                                         double* gdbg, double* hdbg, Ctl* c, double* part,
+                                                         unsigned int* counter) {
+  if (c->status != ST_RUNNING) return;
+  const double rSP = 1.0 / c->SP, invB = c->invB, sigma = c->sigma, ap = c->alpha_prev;
+  const int apply = c->apply_prev;
+  double acc[2] = {-INFINITY, 0.0};
+  constexpr int U = 2;
+  const int64_t chunk = (int64_t)U * MWU_NT;
+  for (int64_t base = (int64_t)blockIdx.x * chunk; base < E; base += (int64_t)gridDim.x * chunk) {
+    double xe[U], dp[U], us[U], ud[U];
+    int sr[U], dr[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t e = base + k * MWU_NT + threadIdx.x;
+      if (e < E) { xe[k] = x[e]; dp[k] = d[e]; sr[k] = __ldg(srow + e); dr[k] = __ldg(drow + e); }
+      else { sr[k] = -1; dr[k] = -1; }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (sr[k] >= 0) { us[k] = __ldg(u + sr[k]); ud[k] = __ldg(u + dr[k]); }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t e = base + k * MWU_NT + threadIdx.x;
+      double de = 0.0;
+      if (e < E) {
+        if (apply && dp[k] != 0.0) { xe[k] = xe[k] + ap * dp[k]; x[e] = xe[k]; }   // P:677 (lazy)
+        const double g = us[k] * rSP + ud[k] * rSP;                                // M^T w_p
+        if (g < invB) de = mwu_direction(g, invB, xe[k], sigma);                   // g >= h: d = 0
+        if (de != dp[k]) d[e] = de;
+        if (gdbg) { gdbg[e] = g; hdbg[e] = invB; }
+        acc[0] = fmax(acc[0], de);
+        acc[1] += invB * de;
+        if (de > 0.0) red_add_f64(dy + dr[k], de);                // dst side
+      }
+      if (__any_sync(0xffffffffu, de > 0.0)) {                    // src side: sorted runs
+        double run;
+        if (warp_run_sum(sr[k], de, run) && run > 0.0) red_add_f64(dy + sr[k], run);
+      }
+    }
+  }
+  const int ops[2] = {OP_MAX, OP_SUM};
+  reduce_and_finalize<2>(acc, ops, part, counter, c, A_COL);
+}
+
+// Init forward product y = P x of the edge-variable kinds by scatter (fast path):
+// MATCH: y_r += x_e for both endpoints (P = M); DENSEST: y_r += (1/D) x_{2e+b} (P = O/D).
+__global__ void scatter_init(int64_t E, const int32_t* __restrict__ srow, const int32_t* __restrict__ drow,
+                             const double* __restrict__ x, double* __restrict__ y, const Ctl* c, int pairs) {
+  const double s = c->invB;
+  for (int64_t e = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; e < E; e += (int64_t)gridDim.x * MWU_NT) {
+    if (pairs) {
+      red_add_f64(y + srow[e], s * x[2 * e]);
+      red_add_f64(y + drow[e], s * x[2 * e + 1]);
+    } else {
+      red_add_f64(y + srow[e], x[e]);
+      red_add_f64(y + drow[e], x[e]);
+    }
+  }
+}
+
 // Rare path of the inactive-row aggregate: when min_inactive z - s_C exceeds 600/eta the sum of
 // v at shift s_C may have lost terms to underflow; recompute it at shift mzi exactly.
 __global__ void __launch_bounds__(MWU_NT) inactive_exact(int64_t E, const uint32_t* __restrict__ act,

@@ -76,13 +76,16 @@ struct mwu_ctx {
   double *colmaxP = nullptr, *colsumC = nullptr, *crecipC = nullptr, *crecipP = nullptr;
   // fast densest path (lazyC): compacted covering-row records per MWU_CT-edge tile
   int lazyC = 0;
+  int scatterP = 0;          // graph kinds with edge variables: d^(y) scattered by the column kernel
+  uint32_t* perm = nullptr;  // scatterP: internal (L2-blocked) edge position -> original edge id
   int64_t ntilesC = 0;
   double *rz = nullptr, *rdz = nullptr, *rv = nullptr;
   int32_t* tcnt = nullptr;
   uint32_t* act = nullptr;   // activity bits of d (bit e: edge e's pair of directions is nonzero)
   // vectors
   double *x = nullptr, *d = nullptr, *y = nullptr, *dy = nullptr, *u = nullptr, *z = nullptr, *dz = nullptr,
-         *v = nullptr, *gtmp = nullptr, *gdbg = nullptr, *hdbg = nullptr, *xbest = nullptr, *tmp = nullptr;
+         *v = nullptr, *gtmp = nullptr, *gdbg = nullptr, *hdbg = nullptr, *xbest = nullptr, *tmp = nullptr,
+         *tmp2 = nullptr;
   Ctl* ctl = nullptr;
   Ctl* hctl = nullptr;  // pinned host mirror
   double* part = nullptr;
@@ -271,6 +274,7 @@ void alloc_vectors(mwu_ctx* c) {
   if (c->mP > mx) mx = c->mP;
   if (c->mC > mx) mx = c->mC;
   c->tmp = dalloc<double>(c, mx);
+  if (c->scatterP) c->tmp2 = dalloc<double>(c, c->n);
   if (c->kind == K_CSR && !c->pSing && !c->cSing) c->gtmp = dalloc<double>(c, c->n);
   CK(cudaMemsetAsync(c->d, 0, c->n * sizeof(double), c->st));
   CK(cudaMemsetAsync(c->x, 0, c->n * sizeof(double), c->st));
@@ -431,6 +435,40 @@ void build_graph_storage(mwu_ctx* c, const mwu_graph* g) {
   if (g->kind == MWU_G_VCOVER) build_plan(c, c->inc_all);
 }
 
+// Fast edge-variable kinds: L2-blocked internal edge order (storage.cuh k_block_keys) and the
+// endpoint rows of the internal order.  perm maps internal -> original edge ids (Q29 order is
+// restored by every vector hook and mwu_get_x).
+constexpr int kBlockL = 22, kBlockR = 20;   // src blocks of 4M vertices, dst blocks of 1M
+void build_blocked_order(mwu_ctx* c) {
+  const int64_t E = c->E;
+  if (E <= 0) return;
+  const int nbL = (int)((c->nv + (int64_t(1) << kBlockL) - 1) >> kBlockL);
+  const int nbR = (int)((c->nv + (int64_t(1) << kBlockR) - 1) >> kBlockR);
+  unsigned long long *keys = talloc<unsigned long long>(E), *kout = talloc<unsigned long long>(E);
+  uint32_t* vals = talloc<uint32_t>(E);
+  c->perm = dalloc<uint32_t>(c, E);
+  k_block_keys<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->src, c->dst, nbR, kBlockL, kBlockR, keys, vals);
+  CKL();
+  int bits = kBlockL + kBlockR;
+  while (bits < 64 && (1ull << (bits - kBlockL - kBlockR)) < (unsigned long long)nbL * (unsigned long long)nbR) ++bits;
+  size_t tb = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, kout, vals, c->perm, E, 0, bits, c->st));
+  void* t = talloc<char>(tb);
+  CK(cub::DeviceRadixSort::SortPairs(t, tb, keys, kout, vals, c->perm, E, 0, bits, c->st));
+  k_map_endpoints_perm<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->perm, c->src, c->dst, c->prow, c->srow, c->drow);
+  CKL();
+  sync(c);
+  tfree(t); tfree(keys); tfree(kout); tfree(vals);
+}
+
+// internal -> original order of an edge-variable (w = 1 match, 2 densest) or edge-row (w = 1) vector
+const double* unperm(mwu_ctx* c, const double* in, int w) {
+  if (!c->perm) return in;
+  k_unperm<<<grid_for(c, c->E), MWU_NT, 0, c->st>>>(c->E, c->perm, in, c->tmp2, w);
+  CKL();
+  return c->tmp2;
+}
+
 // ------------------------------------------------------------------------------ CSR build
 void copy_csr_checked(mwu_ctx* c, const mwu_csr* A, Seg& S, int64_t cols, const char* name) {
   if (A->rows < 0 || A->cols != cols || A->nnz < 0 || !A->rowptr || (A->nnz > 0 && !A->colidx))
@@ -517,6 +555,16 @@ EpColumn make_col(mwu_ctx* c, int s_is_h, const double* gtmp) {
 void enqueue_column(mwu_ctx* c, cudaStream_t st) {
   switch (c->kind) {
     case K_MATCH:
+      if (c->scatterP) {
+        CK(cudaMemsetAsync(c->dy, 0, (c->mP > 0 ? c->mP : 1) * sizeof(double), st));
+        const int64_t blocks = (c->E + 2 * MWU_NT - 1) / (2 * MWU_NT);
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, 3 * c->sms));
+        col_match_fast<<<g, MWU_NT, 0, st>>>(c->E, c->srow, c->drow, c->u, c->x, c->d, c->dy,
+                                            c->record ? c->gdbg : nullptr, c->record ? c->hdbg : nullptr,
+                                            c->ctl, c->part, c->counter);
+        c->launches++;
+        break;
+      }
       col_match<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, c->srow, c->drow, c->u, c->x, c->d,
                                                       c->record ? c->gdbg : nullptr, c->record ? c->hdbg : nullptr,
                                                       c->ctl, c->part, c->counter);
@@ -568,6 +616,17 @@ void enqueue_forward(mwu_ctx* c, cudaStream_t st, const double* in, double* oy, 
   const int a_done = init ? A_NONE : A_STEP_DONE;
   switch (c->kind) {
     case K_MATCH:
+      if (!init && c->scatterP) {            // d^(y) was scattered by the column kernel
+        dy_finalize<<<rows_grid(c, c->mP), MWU_NT, 0, st>>>(c->mP, c->dy, c->ctl, c->part, c->counter);
+        c->launches++;
+        break;
+      }
+      if (init && c->scatterP) {
+        CK(cudaMemsetAsync(oy, 0, (c->mP > 0 ? c->mP : 1) * sizeof(double), st));
+        scatter_init<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, c->srow, c->drow, in, oy, c->ctl, 0);
+        c->launches++;
+        break;
+      }
       launch_seg(c, st, c->inc_p, item_of(c->inc_p, in, 1, nullptr), ey, a_done_p);
       break;
     case K_DENSEST:
@@ -579,6 +638,12 @@ void enqueue_forward(mwu_ctx* c, cudaStream_t st, const double* in, double* oy, 
       if (init) {
         pair_sum<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, in, oz, c->ctl);
         c->launches++;
+      }
+      if (init && c->scatterP) {
+        CK(cudaMemsetAsync(oy, 0, (c->mP > 0 ? c->mP : 1) * sizeof(double), st));
+        scatter_init<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, c->srow, c->drow, in, oy, c->ctl, 1);
+        c->launches++;
+        break;
       }
       launch_seg(c, st, c->inc_p, item_of(c->inc_p, in, 0, invB), ey, a_done_p);
       break;
@@ -1053,6 +1118,7 @@ mwu_status mwu_create_graph(const mwu_graph* g, const mwu_options* opt, mwu_ctx*
       case MWU_G_BMATCH: case MWU_G_MATCH:
         if (g->n_edges == 0) throw MwuError{MWU_ERR_ARG, "matching needs at least one edge"};
         c->kind = K_MATCH; c->mode = MWU_PURE_PACKING; c->n = c->E; c->mP = c->nprime; c->cSing = 1;
+        c->scatterP = c->opt.deterministic ? 0 : 1;
         c->nnzP = 2 * c->E; c->nnzC = c->E; c->empty_dropped = c->nv - c->nprime;
         break;
       case MWU_G_VCOVER:
@@ -1067,9 +1133,11 @@ mwu_status mwu_create_graph(const mwu_graph* g, const mwu_options* opt, mwu_ctx*
         if (g->n_edges == 0) throw MwuError{MWU_ERR_ARG, "densest subgraph needs at least one edge"};
         c->kind = K_DENSEST; c->mode = MWU_MIXED; c->n = 2 * c->E; c->mP = c->nprime; c->mC = c->E;
         c->lazyC = (c->opt.deterministic || c->E >= (int64_t(1) << 31) - MWU_CT) ? 0 : 1;
+        c->scatterP = c->lazyC;
         c->nnzP = 2 * c->E; c->nnzC = 2 * c->E; c->empty_dropped = c->nv - c->nprime;
         break;
     }
+    if (c->scatterP) build_blocked_order(c);
     alloc_vectors(c);
     fill_static_stats(c);
     CK(cudaEventRecord(b, c->st));
@@ -1185,7 +1253,8 @@ mwu_status mwu_get_x(mwu_ctx* c, double* x, int64_t len) {
   GUARD(c);
   if (!x || len != c->n) { c->err = "mwu_get_x: len must equal n"; return MWU_ERR_ARG; }
   try {
-    CK(cudaMemcpyAsync(x, c->xbest, c->n * sizeof(double), cudaMemcpyDefault, c->st));
+    const double* src = unperm(c, c->xbest, c->kind == K_DENSEST ? 2 : 1);
+    CK(cudaMemcpyAsync(x, src, c->n * sizeof(double), cudaMemcpyDefault, c->st));
     sync(c);
   } catch (const MwuError& e) { return fail(c, e); }
   return MWU_OK;
@@ -1298,6 +1367,14 @@ mwu_status mwu_get_vec(mwu_ctx* c, int which, double* out, int64_t len) {
         }
         else { scale_div<<<rows_grid(c, c->mC), MWU_NT, 0, c->st>>>(c->mC, c->v, c->tmp, &c->ctl->SC); CKL(); src = c->tmp; }
         break;
+    }
+    if (c->perm && !use_scal) {              // internal (L2-blocked) edge order -> original (Q29)
+      const int w = (c->kind == K_DENSEST) ? 2 : 1;
+      if (which == MWU_VEC_X || which == MWU_VEC_D || which == MWU_VEC_XBEST || which == MWU_VEC_G ||
+          which == MWU_VEC_H)
+        src = unperm(c, src, w);
+      else if (c->kind == K_DENSEST && (which == MWU_VEC_Z || which == MWU_VEC_DZ || which == MWU_VEC_WC))
+        src = unperm(c, src, 1);
     }
     if (use_scal) CK(cudaMemcpyAsync(out, &scal, sizeof(double), cudaMemcpyDefault, c->st));
     else CK(cudaMemcpyAsync(out, src, L * sizeof(double), cudaMemcpyDefault, c->st));

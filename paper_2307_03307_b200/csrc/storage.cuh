@@ -102,6 +102,39 @@ __global__ void k_map_endpoints(int64_t E, const int32_t* src, const int32_t* ds
   }
 }
 
+// L2-blocked edge order (the paper's CSB blocking, at L2 scale): key = (block pair
+// (src >> BL, dst >> BR), src & maskL, dst & maskR).  A wide src block (2^BL vertices) stays
+// L2-resident (its gathered u and scattered d^(y) slices) while the narrow dst blocks (2^BR)
+// stream past it, so each random-access slice is fetched ~once per src block instead of once
+// per access.
+__global__ void k_block_keys(int64_t E, const int32_t* src, const int32_t* dst, int nbR, int BL, int BR,
+                             unsigned long long* keys, uint32_t* vals) {
+  const unsigned long long mL = (1ull << BL) - 1ull, mR = (1ull << BR) - 1ull;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long a = (unsigned long long)src[e], b = (unsigned long long)dst[e];
+    const unsigned long long pair = (a >> BL) * (unsigned long long)nbR + (b >> BR);
+    keys[e] = (pair << (BL + BR)) | ((a & mL) << BR) | (b & mR);
+    vals[e] = (uint32_t)e;
+  }
+}
+
+__global__ void k_map_endpoints_perm(int64_t E, const uint32_t* perm, const int32_t* src, const int32_t* dst,
+                                     const int32_t* prow, int32_t* srow, int32_t* drow) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t e = perm[i];
+    srow[i] = prow[src[e]];
+    drow[i] = prow[dst[e]];
+  }
+}
+
+// internal (blocked) order -> original order: out[perm[i] * w + b] = in[i * w + b]
+__global__ void k_unperm(int64_t E, const uint32_t* perm, const double* in, double* out, int w) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = (int64_t)perm[i] * w;
+    for (int b = 0; b < w; ++b) out[o + b] = in[i * w + b];
+  }
+}
+
 __global__ void k_domset_keys(int64_t nv, int64_t E, const int32_t* src, const int32_t* dst, unsigned long long* keys) {
   const int64_t tot = nv + 2 * E;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
