@@ -123,6 +123,17 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def ncu_traffic(workload, phase):
+    """DRAM bytes per launch of the phase's dominant kernel from the committed ncu --set full
+    summary (profiles/ncu_traffic.json, written from the captures under gpurun_out/)."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        e = t[workload][phase]
+        return e["dram_bytes_per_launch"], e
+    except Exception:
+        return None, None
+
+
 def measured_peak_gbs():
     try:
         mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -244,8 +255,11 @@ def run_ours(args):
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t0
     gs = graph_stats(G)
-    S = Solver.graph(kind, G.src, G.dst, G.n_vertices, G.n_left if kind == "bmatch" else 0,
-                     max_iter=args.max_iter)
+    # c4 / c5 shard their edges over the ranks (one allreduce of d^(y) per iteration, DESIGN.md
+    # §7); the small configs run one replica per GPU
+    sharded = ws > 1 and args.workload in ("c4", "c5")
+    make = Solver.graph_distributed if sharded else Solver.graph
+    S = make(kind, G.src, G.dst, G.n_vertices, G.n_left if kind == "bmatch" else 0, max_iter=args.max_iter)
     st0 = S.stats()
     L, H, sense = bracket(kind, gs, eps)
 
@@ -304,7 +318,7 @@ def run_ours(args):
     stats = S.stats()
     if rk != 0:
         return 0
-    value = ws * n_done / (ms / 1000.0)
+    value = (1 if sharded else ws) * n_done / (ms / 1000.0)
     nnz_iter = full_nnz(kind, gs)
     pb = phase_bytes(kind, gs)
     peak, peak_kind = measured_peak_gbs()
@@ -339,8 +353,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
-        S2 = Solver.graph(kind, src_h, dst_h, G.n_vertices, G.n_left if kind == "bmatch" else 0,
-                          max_iter=args.max_iter)
+        S2 = make(kind, src_h, dst_h, G.n_vertices, G.n_left if kind == "bmatch" else 0, max_iter=args.max_iter)
         S2.probe_begin(math.sqrt(L * H), eps)
         S = S2
         state.update({"L": L, "H": H, "B": math.sqrt(L * H)})
@@ -350,23 +363,27 @@ def run_ours(args):
         f1.record()
         torch.cuda.synchronize()
         ms2 = f0.elapsed_time(f1)
-        e2e = {"value": n2 / (ms2 / 1000.0), "unit": "iterations/s",
+        e2e = {"value": (1 if sharded else ws) * n2 / (ms2 / 1000.0), "unit": "iterations/s",
                "h2d_bytes_per_step": int(8 * gs["E"] / max(1, n2)), "d2h_bytes_per_step": int(8 * S2.n / max(1, n2)),
                "note": f"create from pinned host edge list + {n2} steps + x to pinned host, {ms2:.1f} ms"}
     line = {
         "metric": "MWU iterations/s", "value": value, "unit": "iterations/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.workload}: {desc}", "kind": kind, "eps": eps, "seed": args.seed,
                    "n_vars": stats["n"], "m_P": stats["m_P"], "m_C": stats["m_C"], "nnz": nnz_iter,
                    "edges": gs["E"], "first_bound": math.sqrt(L * H),
-                   "l2": "inputs larger than L2 (per-vector GBs)", "parallelism": f"replicas x{ws}" if ws > 1 else "1 GPU"},
+                   "l2": "inputs larger than L2 (per-vector GBs)",
+                   "parallelism": (f"edge-sharded x{ws} (NCCL allreduce of d^(y) per iteration)" if sharded
+                                   else (f"replicas x{ws}" if ws > 1 else "1 GPU"))},
         "nnz_per_s": nnz_iter * value,
         "iteration_roofline": {"bytes_alg_per_iter": balg, "achieved_gbs": balg / (ms_per_step / 1000) / 1e9,
                                "frac_of_8TBs": balg / (ms_per_step / 1000) / 8e12,
                                "frac_of_measured": balg / (ms_per_step / 1000) / 1e9 / peak},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": phases[dom]["gbs"], "peak": peak, "unit": "GB/s",
-                     "frac": phases[dom]["gbs"] / peak, "traffic": None, "peak_source": peak_kind},
+                     "frac": phases[dom]["gbs"] / peak, "traffic": ncu_traffic(args.workload, dom)[0],
+                     "traffic_source": (ncu_traffic(args.workload, dom)[1] or {}).get("source"),
+                     "peak_source": peak_kind},
         "phases": phases, "search_passes_per_iter": passes_per_iter,
         "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": int(round(launches_per_iter * n_done)),

@@ -105,6 +105,7 @@ typedef struct {
   int device;            /* CUDA device ordinal; -1 = current device                             */
   int world, rank;       /* multi-GPU: number of ranks and this rank (1, 0 for one GPU)          */
   const void *nccl_id;   /* 128-byte ncclUniqueId from mwu_get_unique_id on rank 0 (world > 1)   */
+  void *comm_group;      /* in-process rank group from mwu_simgroup_create (tests), or NULL       */
   int deterministic;     /* 1: every reduction in a fixed order (run-to-run bit-identical); 0     */
                          /* (default): the forward product of graph kinds is scattered with fp64 */
                          /* atomics into the L2-resident vertex vector (summation order varies   */
@@ -229,9 +230,23 @@ mwu_status mwu_profile_iters(mwu_ctx *ctx, int64_t k, double *out10);
 /* Scalars of the current probe: [eta, sigma, sP, SP, sC, SC, t, alpha_last, evals, passes]. */
 mwu_status mwu_get_scalars(mwu_ctx *ctx, double *out10);
 
-/* ---- multi-GPU ---- */
-/* Write a 128-byte ncclUniqueId (rank 0) to share through torch.distributed. */
+/* ---- multi-GPU ----
+ * Edge-sharded kinds (BMATCH / MATCH / DENSEST with deterministic = 0): every rank passes the
+ * SAME full graph to mwu_create_graph with opt.world = W, opt.rank = r; the library orders the
+ * edges (L2-blocked internal order) and keeps the contiguous internal range mwu_shard_range(E,
+ * W, r); the packing (vertex) rows are replicated and the scattered forward product is
+ * sum-allreduced once per iteration.  Every later call (solve, probe hooks, vector hooks,
+ * mwu_get_x) is collective: all ranks call it in the same order; vectors are returned whole on
+ * every rank.  Other kinds return MWU_ERR_ARG for W > 1. */
+/* Write a 128-byte ncclUniqueId (rank 0) to share through torch.distributed.  MWU_ERR_NCCL if
+ * the NCCL library (libnccl.so.2 or $MWU_NCCL_LIB) cannot be loaded. */
 mwu_status mwu_get_unique_id(void *out128);
+/* [*e0, *e1): the internal edge range rank `rank` of `world` owns (host-only, no device work). */
+mwu_status mwu_shard_range(int64_t n_edges, int world, int rank, int64_t *e0, int64_t *e1);
+/* In-process group of `world` ranks on one device (one host thread per rank, host barriers; for
+ * testing the sharded engine without several GPUs).  Pass it as opt.comm_group. */
+mwu_status mwu_simgroup_create(int world, void **group);
+void mwu_simgroup_destroy(void *group);
 
 #ifdef __cplusplus
 }

@@ -24,7 +24,7 @@ constexpr int kWarpSeg = MWU_CT / (MWU_NT / 32);   // edges (and record slots) p
 
 enum Status : int { ST_RUNNING = 0, ST_FEASIBLE = 1, ST_INFEASIBLE = 2, ST_ITER_LIMIT = 3 };
 enum Reason : int { R_NONE = 0, R_MAXD_ZERO = 1, R_ALPHA_LT_1 = 2, R_EMPTY_COVER = 3, R_ITER_LIMIT = 4, R_MIN_Z = 5 };
-enum RedOp : int { OP_SUM = 0, OP_MAX = 1, OP_MIN = 2 };
+enum RedOp : int { OP_SUM = 0, OP_MAX = 1, OP_MIN = 2, OP_FIRST = 3 };
 // candidate evaluation modes of one side in a search pass (DESIGN.md §3 Q16)
 enum CandMode : int { CM_EXPM1 = 0, CM_LSE = 1, CM_EXT = 2 };
 // search phases (Alg. 3)
@@ -93,6 +93,11 @@ struct Ctl {
   int64_t evals_total, passes_total;
   double alpha_last;
   double scratch[MWU_SLOTS];
+  // ---- multi-GPU: partial phase reductions are deferred to the host-driven exchange
+  int32_t world, dpending;             // ranks; a deferred reduction awaits finalize_multi
+  int32_t dn, daction;                 // its slot count and action
+  double dslots[MWU_SLOTS];            // this rank's reduced slots
+  int32_t dops[MWU_SLOTS];             // their combine ops
   // ---- CUDA graph conditional handles (0 when host-driven)
   unsigned long long h_iter, h_search;
   int32_t nan_flag, pad_;

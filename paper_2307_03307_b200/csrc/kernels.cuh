@@ -395,6 +395,43 @@ __device__ void finalize(Ctl* c, int action, double* r) {
   }
 }
 
+// Phase reductions over rank-local rows are partial on a sharded run: the last block parks its
+// reduced slots in the control block and the host exchanges them (allgather) before
+// finalize_multi combines them in rank order and runs the same control logic on every rank.
+__device__ __forceinline__ bool partial_action(int a) {
+  return a == A_COL || a == A_COL_FAST || a == A_SEARCH || a == A_INIT_SING || a == A_INIT_EXT ||
+         a == A_INIT_W || a == A_VI_EXACT || a == A_SUM;
+}
+__device__ void finish(Ctl* c, int action, double* res, const int* ops, int n) {
+  if (c->world > 1 && partial_action(action)) {
+    for (int s = 0; s < n; ++s) { c->dslots[s] = res[s]; c->dops[s] = ops[s]; }
+    c->dn = n;
+    c->daction = action;
+    c->dpending = 1;
+    return;
+  }
+  finalize(c, action, res);
+}
+
+__global__ void finalize_multi(Ctl* c, const double* __restrict__ g, int world) {
+  if (threadIdx.x != 0 || !c->dpending) return;
+  c->dpending = 0;
+  double res[MWU_SLOTS];
+  const int n = c->dn, act = c->daction;
+  for (int s = 0; s < MWU_SLOTS; ++s) res[s] = 0.0;
+  for (int s = 0; s < n; ++s) {
+    int op = c->dops[s];
+    if (act == A_INIT_W && s == 0) op = OP_FIRST;     // S_P of the replicated packing rows
+    double a = g[s];
+    for (int r = 1; r < world; ++r) {
+      const double b = g[(size_t)r * MWU_SLOTS + s];
+      a = (op == OP_FIRST) ? a : red_combine(op, a, b);
+    }
+    res[s] = a;
+  }
+  finalize(c, act, res);
+}
+
 // Standard epilogue of a reducing kernel: block partials -> last block -> finalize.
 template <int NS>
 __device__ __forceinline__ void reduce_and_finalize(double (&acc)[NS], const int* ops, double* part,
@@ -402,7 +439,7 @@ __device__ __forceinline__ void reduce_and_finalize(double (&acc)[NS], const int
   __shared__ double res[MWU_SLOTS];
   block_partials<NS>(acc, ops, part);
   if (last_block_combine(ops, NS, part, counter, res)) {
-    if (threadIdx.x == 0) finalize(c, action, res);
+    if (threadIdx.x == 0) finish(c, action, res, ops, NS);
   }
 }
 
@@ -955,7 +992,7 @@ __device__ __forceinline__ void for_compact_rows(const double* __restrict__ rz, 
 }
 
 struct SearchArgs {
-  int64_t mP; const double *y, *dy, *u;
+  int64_t mP; const double *y, *dy, *u;                  // this rank's slice of the packing rows
   int64_t mC; const double *z, *dz, *v;                  // dense covering rows (v: weights)
   const double *rz, *rdz, *rv; const int32_t* tcnt; int64_t ntiles;   // compacted (rz != nullptr)
 };
@@ -1061,7 +1098,7 @@ __global__ void __launch_bounds__(MWU_NT, 2) search_pass(SearchArgs A, Ctl* c, d
 #pragma unroll
   for (int s = 0; s < MWU_SLOTS; ++s) ops[s] = search_slot_op(s);
   if (last_block_combine(ops, MWU_SLOTS, part, counter, res)) {
-    if (threadIdx.x == 0) finalize(c, A_SEARCH, res);
+    if (threadIdx.x == 0) finish(c, A_SEARCH, res, ops, MWU_SLOTS);
   }
 }
 
@@ -1116,8 +1153,9 @@ __global__ void __launch_bounds__(MWU_NT) init_ext(int64_t mP, const double* __r
 // Init: x_i = eps / (n ||P_{:,i}||_inf); colmax == nullptr: all columns have max cm
 // (graph operators: 1, O/D: 1/D, embedded row: 1/M).  Reduces sum(x/M) for a singleton side.
 __global__ void __launch_bounds__(MWU_NT) init_x(int64_t n, double* __restrict__ x, const double* __restrict__ colmax,
-                                                 double cm, Ctl* c, double* part, unsigned int* counter) {
-  const double eps = c->eps, nd = (double)n, invB = c->invB;
+                                                 double cm, Ctl* c, double* part, unsigned int* counter,
+                                                 int64_t n_all) {
+  const double eps = c->eps, nd = (double)n_all, invB = c->invB;   // n = #variables of the LP (Q3)
   double acc[1] = {0.0};
   for (int64_t i = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * MWU_NT) {
     const double ci = colmax ? colmax[i] : cm;

@@ -3,6 +3,7 @@
 #include "../../include/mwu.h"
 #include "kernels.cuh"
 #include "storage.cuh"
+#include "comm.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -78,6 +79,14 @@ struct mwu_ctx {
   int lazyC = 0;
   int scatterP = 0;          // graph kinds with edge variables: d^(y) scattered by the column kernel
   uint32_t* perm = nullptr;  // scatterP: internal (L2-blocked) edge position -> original edge id
+  // multi-GPU (edge-sharded): this rank owns internal edges [e0, e0 + E)
+  int world = 1, rank = 0;
+  Comm* comm = nullptr;
+  int64_t Eg = 0, ng = 0, mCg = 0, e0 = 0;   // global edges / variables / covering rows
+  uint32_t* perm_full = nullptr;
+  double* gslots = nullptr;                   // [world][MWU_SLOTS] gathered reduction slots
+  double* gfull = nullptr;                    // full internal-order vector (hooks)
+  double* gsend = nullptr;                    // padded local slice (hooks)
   int64_t ntilesC = 0;
   double *rz = nullptr, *rdz = nullptr, *rv = nullptr;
   int32_t* tcnt = nullptr;
@@ -274,7 +283,7 @@ void alloc_vectors(mwu_ctx* c) {
   if (c->mP > mx) mx = c->mP;
   if (c->mC > mx) mx = c->mC;
   c->tmp = dalloc<double>(c, mx);
-  if (c->scatterP) c->tmp2 = dalloc<double>(c, c->n);
+  if (c->scatterP) c->tmp2 = dalloc<double>(c, c->ng > 0 ? c->ng : c->n);
   if (c->kind == K_CSR && !c->pSing && !c->cSing) c->gtmp = dalloc<double>(c, c->n);
   CK(cudaMemsetAsync(c->d, 0, c->n * sizeof(double), c->st));
   CK(cudaMemsetAsync(c->x, 0, c->n * sizeof(double), c->st));
@@ -285,6 +294,17 @@ void alloc_vectors(mwu_ctx* c) {
 
 void init_ctx_common(mwu_ctx* c, const mwu_options* opt) {
   if (opt) c->opt = *opt; else mwu_default_options(&c->opt);
+  c->world = c->opt.world > 1 ? c->opt.world : 1;
+  c->rank = c->world > 1 ? c->opt.rank : 0;
+  if (c->world > 1) {
+    if (c->rank < 0 || c->rank >= c->world) throw MwuError{MWU_ERR_ARG, "rank out of range"};
+    c->opt.use_graph = 0;                    // collectives are host-orchestrated
+    try {
+      if (c->opt.comm_group) c->comm = new SimComm((SimGroup*)c->opt.comm_group, c->rank);
+      else if (c->opt.nccl_id) c->comm = new NcclComm(c->world, c->rank, c->opt.nccl_id);
+      else throw std::runtime_error("world > 1 needs nccl_id or comm_group");
+    } catch (const std::exception& e) { throw MwuError{MWU_ERR_NCCL, e.what()}; }
+  }
   if (c->opt.device >= 0) CK(cudaSetDevice(c->opt.device));
   CK(cudaGetDevice(&c->dev));
   CK(cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->dev));
@@ -435,6 +455,67 @@ void build_graph_storage(mwu_ctx* c, const mwu_graph* g) {
   if (g->kind == MWU_G_VCOVER) build_plan(c, c->inc_all);
 }
 
+// ------------------------------------------------------------------------------ multi-GPU
+void shard_range(int64_t n, int world, int rank, int64_t& a, int64_t& b) {
+  a = (int64_t)((__int128)n * rank / world);
+  b = (int64_t)((__int128)n * (rank + 1) / world);
+}
+
+// complete a deferred partial reduction: gather every rank's slots, combine in rank order
+void exchange(mwu_ctx* c) {
+  if (c->world <= 1) return;
+  try {
+    c->comm->allgather(c->ctl->dslots, c->gslots, MWU_SLOTS, c->st);
+  } catch (const std::exception& e) { throw MwuError{MWU_ERR_NCCL, e.what()}; }
+  finalize_multi<<<1, 32, 0, c->st>>>(c->ctl, c->gslots, c->world);
+  CKL();
+}
+
+void allreduce_rows(mwu_ctx* c, double* v, int64_t n) {
+  if (c->world <= 1) return;
+  try {
+    c->comm->allreduce_sum(v, n, c->st);
+  } catch (const std::exception& e) { throw MwuError{MWU_ERR_NCCL, e.what()}; }
+}
+
+// Restrict the context to this rank's internal edge range (after the global structure build).
+void localize(mwu_ctx* c) {
+  const int w = (c->kind == K_DENSEST) ? 2 : 1;
+  c->Eg = c->E; c->ng = c->n; c->mCg = c->mC;
+  c->perm_full = c->perm;
+  if (c->world <= 1) return;
+  int64_t a, b;
+  shard_range(c->Eg, c->world, c->rank, a, b);
+  c->e0 = a;
+  c->E = b - a;
+  c->n = w * c->E;
+  if (c->kind == K_DENSEST) c->mC = c->E;
+  c->srow += a;
+  c->drow += a;
+  c->perm += a;
+  c->gslots = dalloc<double>(c, (int64_t)c->world * MWU_SLOTS);
+}
+
+// full internal-order vector of an edge-indexed quantity (w per edge) from every rank's slice
+const double* gather_full(mwu_ctx* c, const double* local, int w) {
+  if (c->world <= 1) return local;
+  int64_t maxE = 0;
+  for (int r = 0; r < c->world; ++r) { int64_t a, b; shard_range(c->Eg, c->world, r, a, b); maxE = std::max(maxE, b - a); }
+  if (!c->gfull) { c->gfull = dalloc<double>(c, w * c->Eg); c->gsend = dalloc<double>(c, w * maxE * c->world + w * maxE); }
+  double* recv = c->gsend + w * maxE;
+  CK(cudaMemcpyAsync(c->gsend, local, w * c->E * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+  try {
+    c->comm->allgather(c->gsend, recv, w * maxE, c->st);
+  } catch (const std::exception& e) { throw MwuError{MWU_ERR_NCCL, e.what()}; }
+  for (int r = 0; r < c->world; ++r) {
+    int64_t a, b;
+    shard_range(c->Eg, c->world, r, a, b);
+    if (b > a) CK(cudaMemcpyAsync(c->gfull + w * a, recv + (int64_t)r * w * maxE, w * (b - a) * sizeof(double),
+                                  cudaMemcpyDeviceToDevice, c->st));
+  }
+  return c->gfull;
+}
+
 // Fast edge-variable kinds: L2-blocked internal edge order (storage.cuh k_block_keys) and the
 // endpoint rows of the internal order.  perm maps internal -> original edge ids (Q29 order is
 // restored by every vector hook and mwu_get_x).
@@ -464,7 +545,8 @@ void build_blocked_order(mwu_ctx* c) {
 // internal -> original order of an edge-variable (w = 1 match, 2 densest) or edge-row (w = 1) vector
 const double* unperm(mwu_ctx* c, const double* in, int w) {
   if (!c->perm) return in;
-  k_unperm<<<grid_for(c, c->E), MWU_NT, 0, c->st>>>(c->E, c->perm, in, c->tmp2, w);
+  in = gather_full(c, in, w);
+  k_unperm<<<grid_for(c, c->Eg), MWU_NT, 0, c->st>>>(c->Eg, c->perm_full, in, c->tmp2, w);
   CKL();
   return c->tmp2;
 }
@@ -671,7 +753,13 @@ void enqueue_search(mwu_ctx* c, cudaStream_t st) {
   const int64_t chunks = (std::max(c->mP, c->mC) + MWU_SCH - 1) / MWU_SCH;
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>(2 * c->sms, chunks));   // 2 CTAs / SM
   SearchArgs A;
-  A.mP = c->mP; A.y = c->y; A.dy = c->dy; A.u = c->u;
+  int64_t p0 = 0, p1 = c->mP;                // sharded: each rank sums a slice of the replicated rows
+  if (c->world > 1) {
+    shard_range(c->mP, c->world, c->rank, p0, p1);
+    p0 &= ~int64_t(1);                       // 16-byte aligned bulk copies
+    if (c->rank + 1 < c->world) p1 &= ~int64_t(1);
+  }
+  A.mP = p1 - p0; A.y = c->y + p0; A.dy = c->dy + p0; A.u = c->u + p0;
   A.mC = c->mC; A.z = c->z; A.dz = c->dz; A.v = c->v;
   A.rz = c->rz; A.rdz = c->rdz; A.rv = c->rv; A.tcnt = c->tcnt; A.ntiles = c->ntilesC;
   search_pass<<<g, MWU_NT, kSearchSmem, st>>>(A, c->ctl, c->part, c->counter);
@@ -741,7 +829,7 @@ void build_probe_graph(mwu_ctx* c) {
 }
 
 // ------------------------------------------------------------------------------ probe engine
-int64_t m_total(mwu_ctx* c) { return (c->pSing ? 1 : c->mP) + (c->cSing ? 1 : c->mC); }
+int64_t m_total(mwu_ctx* c) { return (c->pSing ? 1 : c->mP) + (c->cSing ? 1 : (c->mCg > 0 ? c->mCg : c->mC)); }
 
 void probe_begin(mwu_ctx* c, double bound, double eps) {
   if (!(eps > 0.0 && eps < 1.0)) throw MwuError{MWU_ERR_ARG, "eps must be in (0, 1)"};
@@ -765,6 +853,7 @@ void probe_begin(mwu_ctx* c, double bound, double eps) {
   h.bisect_depth = c->opt.bisect_depth;
   h.use_graph = c->opt.use_graph;
   h.lazyC = c->lazyC;
+  h.world = c->world;
   h.status = c->empty_cover ? ST_INFEASIBLE : ST_RUNNING;
   h.reason = c->empty_cover ? R_EMPTY_COVER : R_NONE;
   h.record = c->record;
@@ -779,14 +868,19 @@ void probe_begin(mwu_ctx* c, double bound, double eps) {
   if (c->kind == K_DENSEST) cm = h.invB;                          // P = O/D
   else if (c->kind == K_VCOVER || c->kind == K_DOMSET) cm = h.invB; // P = (1/M)1^T
   else if (c->kind == K_CSR) { if (c->pSing) cm = h.invB; else colmax = c->colmaxP; }
-  init_x<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->x, colmax, cm, c->ctl, c->part, c->counter);
+  init_x<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->x, colmax, cm, c->ctl, c->part, c->counter,
+                                                  c->ng > 0 ? c->ng : c->n);
   c->launches++;
   CKL();
+  exchange(c);
   // y = P x, z = C x
   enqueue_forward(c, c->st, c->x, c->y, c->z, true);
+  allreduce_rows(c, c->y, c->mP);            // sharded: partial packing rows of the local edges
   init_ext<<<rows_grid(c, c->mP + c->mC), MWU_NT, 0, c->st>>>(c->mP, c->y, c->mC, c->z, c->ctl, c->part, c->counter);
   c->launches++;
+  exchange(c);
   enqueue_update(c, c->st, 0);
+  exchange(c);
   CKL();
   sync(c);
   c->probe_active = true;
@@ -800,12 +894,21 @@ void host_iteration(mwu_ctx* c, double alpha) {
   pull_ctl(c);
   if (c->hctl->status != ST_RUNNING) return;
   enqueue_column(c, c->st);
+  if (c->world > 1) {
+    allreduce_rows(c, c->dy, c->mP);         // the one vector exchange per iteration
+    exchange(c);                             // column reductions (max d, sums, inactive rows)
+    if (c->lazyC) {
+      inactive_exact<<<rows_grid(c, c->E), MWU_NT, 0, c->st>>>(c->E, c->act, c->z, c->ctl, c->part, c->counter);
+      exchange(c);
+    }
+  }
   enqueue_forward(c, c->st, c->d, c->dy, c->dz, false);
   CKL();
   for (int guard = 0; guard < 100000; ++guard) {
     pull_ctl(c);
     if (c->hctl->status != ST_RUNNING || !c->hctl->sactive) break;
     enqueue_search(c, c->st);
+    exchange(c);
     CKL();
   }
   enqueue_update(c, c->st, 1);
@@ -871,12 +974,22 @@ void profile_iters(mwu_ctx* c, int64_t k, double* out) {
   for (int64_t it = 0; it < k; ++it) {
     pull_ctl(c);
     if (c->hctl->status != ST_RUNNING) break;
-    timed(0, [&] { enqueue_column(c, c->st); });
+    timed(0, [&] {
+      enqueue_column(c, c->st);
+      if (c->world > 1) {
+        allreduce_rows(c, c->dy, c->mP);
+        exchange(c);
+        if (c->lazyC) {
+          inactive_exact<<<rows_grid(c, c->E), MWU_NT, 0, c->st>>>(c->E, c->act, c->z, c->ctl, c->part, c->counter);
+          exchange(c);
+        }
+      }
+    });
     timed(1, [&] { enqueue_forward(c, c->st, c->d, c->dy, c->dz, false); });
     for (int guard = 0; guard < 100000; ++guard) {
       pull_ctl(c);
       if (c->hctl->status != ST_RUNNING || !c->hctl->sactive) break;
-      timed(2, [&] { enqueue_search(c, c->st); });
+      timed(2, [&] { enqueue_search(c, c->st); exchange(c); });
       out[9] += 1;
     }
     timed(3, [&] { enqueue_update(c, c->st, 1); });
@@ -899,6 +1012,7 @@ void flush(mwu_ctx* c) {
 void reduce_dev(mwu_ctx* c, const double* a, int64_t n, double& sum, double& mx) {
   reduce_vec<<<rows_grid(c, n), MWU_NT, 0, c->st>>>(n, a, c->ctl, c->part, c->counter);
   CKL();
+  exchange(c);
   double s[2];
   CK(cudaMemcpyAsync(s, c->ctl->scratch, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
   sync(c);
@@ -910,7 +1024,7 @@ void reduce_dev(mwu_ctx* c, const double* a, int64_t n, double& sum, double& mx)
 void brackets(mwu_ctx* c, double eps, double& L, double& H) {
   double s, mx;
   if (c->kind == K_DENSEST) {
-    L = (double)c->E / (double)c->nprime;
+    L = (double)(c->Eg > 0 ? c->Eg : c->E) / (double)c->nprime;
     H = (double)c->maxdeg / 2.0;
     k_fill<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->xbest, 0.5);
     CKL();
@@ -936,12 +1050,14 @@ void brackets(mwu_ctx* c, double eps, double& L, double& H) {
   // packing: witness x0 / max(P x0) (x0 of P:272), H = sum_i max_j 1/p_ji
   Ctl& h = *c->hctl;
   memset(&h, 0, sizeof(Ctl));
-  h.eps = eps; h.invB = 1.0; h.status = ST_RUNNING; h.iter_stop = INT64_MAX;
+  h.eps = eps; h.invB = 1.0; h.status = ST_RUNNING; h.iter_stop = INT64_MAX; h.world = c->world;
   CK(cudaMemcpyAsync(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, c->st));
   init_x<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->x, c->kind == K_CSR ? c->colmaxP : nullptr, 1.0, c->ctl,
-                                                  c->part, c->counter);
+                                                  c->part, c->counter, c->ng > 0 ? c->ng : c->n);
   CKL();
+  exchange(c);
   enqueue_forward(c, c->st, c->x, c->y, c->z, true);
+  allreduce_rows(c, c->y, c->mP);
   reduce_dev(c, c->y, c->mP, s, mx);
   CK(cudaMemcpyAsync(c->tmp, &mx, sizeof(double), cudaMemcpyHostToDevice, c->st));
   scale_div<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->x, c->xbest, c->tmp);
@@ -949,7 +1065,7 @@ void brackets(mwu_ctx* c, double eps, double& L, double& H) {
   sync(c);
   reduce_dev(c, c->xbest, c->n, s, mx);
   L = s;
-  if (c->kind == K_MATCH) H = (double)c->E;
+  if (c->kind == K_MATCH) H = (double)(c->Eg > 0 ? c->Eg : c->E);
   else { reduce_dev(c, c->crecipP, c->n, s, mx); H = s; }
 }
 
@@ -1064,6 +1180,7 @@ mwu_status fail(mwu_ctx* c, const MwuError& e) {
 
 void destroy_ctx(mwu_ctx* c) {
   if (!c) return;
+  if (c->comm) { delete c->comm; c->comm = nullptr; }
   if (c->gexec) cudaGraphExecDestroy(c->gexec);
   if (c->graph) cudaGraphDestroy(c->graph);
   if (c->st) cudaStreamSynchronize(c->st);
@@ -1094,6 +1211,7 @@ void mwu_default_options(mwu_options* o) {
   o->world = 1;
   o->rank = 0;
   o->nccl_id = nullptr;
+  o->comm_group = nullptr;
   o->deterministic = 0;
 }
 
@@ -1138,8 +1256,11 @@ mwu_status mwu_create_graph(const mwu_graph* g, const mwu_options* opt, mwu_ctx*
         break;
     }
     if (c->scatterP) build_blocked_order(c);
+    fill_static_stats(c);                    // global sizes
+    if (c->world > 1 && !c->scatterP)
+      throw MwuError{MWU_ERR_ARG, "multi-GPU sharding needs an edge-variable kind (bmatch, match, densest) with deterministic = 0"};
+    localize(c);
     alloc_vectors(c);
-    fill_static_stats(c);
     CK(cudaEventRecord(b, c->st));
     CK(cudaEventSynchronize(b));
     float ms = 0; CK(cudaEventElapsedTime(&ms, a, b));
@@ -1251,10 +1372,11 @@ mwu_status mwu_solve(mwu_ctx* c, double eps, int64_t max_iter, int32_t* outcome)
 
 mwu_status mwu_get_x(mwu_ctx* c, double* x, int64_t len) {
   GUARD(c);
-  if (!x || len != c->n) { c->err = "mwu_get_x: len must equal n"; return MWU_ERR_ARG; }
+  const int64_t n = c->ng > 0 ? c->ng : c->n;
+  if (!x || len != n) { c->err = "mwu_get_x: len must equal n"; return MWU_ERR_ARG; }
   try {
     const double* src = unperm(c, c->xbest, c->kind == K_DENSEST ? 2 : 1);
-    CK(cudaMemcpyAsync(x, src, c->n * sizeof(double), cudaMemcpyDefault, c->st));
+    CK(cudaMemcpyAsync(x, src, n * sizeof(double), cudaMemcpyDefault, c->st));
     sync(c);
   } catch (const MwuError& e) { return fail(c, e); }
   return MWU_OK;
@@ -1307,11 +1429,12 @@ mwu_status mwu_run_probe(mwu_ctx* c, int32_t* state) { return mwu_run_iters(c, -
 
 int64_t mwu_vec_len(mwu_ctx* c, int which) {
   if (!c) return 0;
+  const int64_t n = c->ng > 0 ? c->ng : c->n, mC = c->mCg > 0 ? c->mCg : c->mC;   // whole vectors
   switch (which) {
-    case MWU_VEC_X: case MWU_VEC_D: case MWU_VEC_XBEST: return c->n;
-    case MWU_VEC_G: case MWU_VEC_H: return c->record ? c->n : 0;
+    case MWU_VEC_X: case MWU_VEC_D: case MWU_VEC_XBEST: return n;
+    case MWU_VEC_G: case MWU_VEC_H: return c->record ? n : 0;
     case MWU_VEC_Y: case MWU_VEC_DY: case MWU_VEC_WP: return c->pSing ? 1 : c->mP;
-    case MWU_VEC_Z: case MWU_VEC_DZ: case MWU_VEC_WC: return c->cSing ? 1 : c->mC;
+    case MWU_VEC_Z: case MWU_VEC_DZ: case MWU_VEC_WC: return c->cSing ? 1 : mC;
   }
   return 0;
 }
@@ -1453,8 +1576,31 @@ mwu_status mwu_profile_iters(mwu_ctx* c, int64_t k, double* out10) {
 }
 
 mwu_status mwu_get_unique_id(void* out128) {
-  (void)out128;
-  return MWU_ERR_NCCL;
+  if (!out128) return MWU_ERR_ARG;
+  try {
+    NcclLib& L = NcclLib::get();
+    NcclUid id;
+    if (L.getUniqueId(&id) != 0) { g_create_err = "ncclGetUniqueId failed"; return MWU_ERR_NCCL; }
+    memcpy(out128, id.internal, 128);
+  } catch (const std::exception& e) {
+    g_create_err = e.what();
+    return MWU_ERR_NCCL;
+  }
+  return MWU_OK;
 }
+
+mwu_status mwu_shard_range(int64_t n, int world, int rank, int64_t* e0, int64_t* e1) {
+  if (!e0 || !e1 || n < 0 || world < 1 || rank < 0 || rank >= world) return MWU_ERR_ARG;
+  shard_range(n, world, rank, *e0, *e1);
+  return MWU_OK;
+}
+
+mwu_status mwu_simgroup_create(int world, void** group) {
+  if (!group || world < 1) return MWU_ERR_ARG;
+  *group = new SimGroup(world);
+  return MWU_OK;
+}
+
+void mwu_simgroup_destroy(void* group) { delete (SimGroup*)group; }
 
 }  // extern "C"

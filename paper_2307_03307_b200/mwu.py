@@ -44,7 +44,8 @@ class Options(ctypes.Structure):
     _fields_ = [("eta_factor", ctypes.c_double), ("max_iter", ctypes.c_int64), ("tol_prose", ctypes.c_int),
                 ("max_evals", ctypes.c_int), ("outer_rel_tol", ctypes.c_double), ("use_graph", ctypes.c_int),
                 ("bisect_depth", ctypes.c_int), ("device", ctypes.c_int), ("world", ctypes.c_int),
-                ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p), ("deterministic", ctypes.c_int)]
+                ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p), ("comm_group", ctypes.c_void_p),
+                ("deterministic", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -61,7 +62,8 @@ class Stats(ctypes.Structure):
 EXPORTS = ["mwu_default_options", "mwu_create_csr", "mwu_create_graph", "mwu_solve", "mwu_get_x",
            "mwu_get_stats", "mwu_destroy", "mwu_last_error", "mwu_probe_begin", "mwu_step", "mwu_run_probe",
            "mwu_run_iters", "mwu_get_vec", "mwu_vec_len", "mwu_set_record", "mwu_get_structure",
-           "mwu_get_scalars", "mwu_get_unique_id", "mwu_profile_iters"]
+           "mwu_get_scalars", "mwu_get_unique_id", "mwu_profile_iters", "mwu_shard_range",
+           "mwu_simgroup_create", "mwu_simgroup_destroy"]
 
 _lib = None
 
@@ -99,20 +101,69 @@ def lib():
         L.mwu_get_scalars.argtypes = [vp, ctypes.POINTER(dbl)]
         L.mwu_get_unique_id.argtypes = [vp]
         L.mwu_profile_iters.argtypes = [vp, i64, ctypes.POINTER(dbl)]
+        L.mwu_shard_range.argtypes = [i64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+        L.mwu_simgroup_create.argtypes = [ctypes.c_int, ctypes.POINTER(vp)]
+        L.mwu_simgroup_destroy.argtypes = [vp]
+        L.mwu_simgroup_destroy.restype = None
         for name in EXPORTS:
             getattr(L, name)
         _lib = L
     return _lib
 
 
-def default_options(**kw) -> Options:
+def default_options(keep=None, **kw) -> Options:
     o = Options()
     lib().mwu_default_options(ctypes.byref(o))
     for k, v in kw.items():
         if not hasattr(o, k):
             raise TypeError(f"unknown option {k}")
+        if k == "nccl_id" and isinstance(v, (bytes, bytearray)):
+            buf = ctypes.create_string_buffer(bytes(v), 128)
+            if keep is not None:
+                keep.append(buf)
+            v = ctypes.cast(buf, ctypes.c_void_p)
+        elif k == "comm_group" and isinstance(v, SimGroup):
+            v = v.handle
         setattr(o, k, v)
     return o
+
+
+def get_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it; share it with torch.distributed)."""
+    buf = ctypes.create_string_buffer(128)
+    st = lib().mwu_get_unique_id(buf)
+    if st != OK:
+        raise MwuError(f"mwu_get_unique_id: status {st}: {lib().mwu_last_error(None).decode()}")
+    return buf.raw
+
+
+def share_unique_id(make_id) -> bytes:
+    """Rank 0 calls make_id() and every rank of the torch.distributed group receives it."""
+    import torch.distributed as dist
+    box = [make_id() if dist.get_rank() == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    return box[0]
+
+
+def shard_range(n_edges: int, world: int, rank: int):
+    """The internal edge range [e0, e1) rank `rank` of `world` owns (mwu_shard_range)."""
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().mwu_shard_range(int(n_edges), int(world), int(rank), ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
+
+
+class SimGroup:
+    """In-process group of `world` ranks on one device (tests of the sharded engine)."""
+
+    def __init__(self, world: int):
+        h = ctypes.c_void_p()
+        _check(lib().mwu_simgroup_create(int(world), ctypes.byref(h)))
+        self.handle, self.world = h, world
+
+    def close(self):
+        if self.handle:
+            lib().mwu_simgroup_destroy(self.handle)
+            self.handle = None
 
 
 def _ptr(t: torch.Tensor | None):
@@ -140,10 +191,20 @@ class Solver:
         src = src.to(torch.int32).contiguous()
         dst = dst.to(torch.int32).contiguous()
         g = _Graph(GRAPH_KINDS[kind], int(n_vertices), int(src.numel()), int(n_left), _ptr(src), _ptr(dst))
-        o = default_options(**opts)
+        keep = [src, dst]
+        o = default_options(keep, **opts)
         h = ctypes.c_void_p()
         _check(lib().mwu_create_graph(ctypes.byref(g), ctypes.byref(o), ctypes.byref(h)))
-        return cls(h, (src, dst))
+        return cls(h, keep)
+
+    @classmethod
+    def graph_distributed(cls, kind: str, src, dst, n_vertices: int, n_left: int = 0, **opts) -> "Solver":
+        """Edge-sharded context over the torch.distributed process group (one GPU per rank):
+        rank 0 creates the NCCL id, every rank passes the same full edge list."""
+        import torch.distributed as dist
+        ws, rk = dist.get_world_size(), dist.get_rank()
+        uid = share_unique_id(get_unique_id)
+        return cls.graph(kind, src, dst, n_vertices, n_left, world=ws, rank=rk, nccl_id=uid, **opts)
 
     @classmethod
     def csr(cls, mode: int, n: int, P=None, C=None, **opts) -> "Solver":
