@@ -13,7 +13,7 @@
 #define MWU_NT 256            // threads per block for every kernel
 #define MWU_MAXC 8            // step-search candidates evaluated per HBM pass
 #define MWU_SLOTS 48          // reduction slots per block partial (6 * MAXC)
-#define MWU_CT 512            // edges per column tile (compacted covering-row records)
+#define MWU_CT 1024           // edges per column tile (compacted covering-row records)
 #define MWU_TILE 2048         // items per seg tile (a tile loads <= 2*TILE items into smem)
 #define MWU_LCH 8192          // items per chunk of a long row (deg > TILE)
 
@@ -89,6 +89,9 @@ struct Ctl {
   int32_t cexp[MWU_MAXC], csq[MWU_MAXC];
   double cand[MWU_MAXC], cea[MWU_MAXC], shP[MWU_MAXC], shC[MWU_MAXC];
   int32_t cmP[MWU_MAXC], cmC[MWU_MAXC];
+  // ---- first-window guesses: accepted step sizes of the previous probe at the same iteration
+  // index (only a choice of which candidates the first search pass evaluates)
+  double aguess[32], ahist[32];
   // ---- statistics (accumulated over the probe)
   int64_t evals_total, passes_total;
   double alpha_last;
@@ -197,6 +200,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   }
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// 8-byte asynchronous gather global -> shared (LDGSTS): the loaded value never occupies a
+// register, so a gather issued one tile ahead cannot stall the issuing warp
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }

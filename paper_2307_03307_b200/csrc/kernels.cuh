@@ -16,6 +16,9 @@
 #pragma once
 #include "common.cuh"
 #include "fastmath.cuh"
+#ifndef MWU_ABLATE
+#define MWU_ABLATE 0
+#endif
 
 namespace mwu {
 
@@ -97,7 +100,8 @@ __device__ void stage_double_first(Ctl* c) {
   c->dk_lo = -1;
   c->dk_hi = 1 << 20;
   int kg = 1;
-  if (c->t > 0 && c->alpha_prev >= 1.0) kg = ilogb(c->alpha_prev);
+  if (c->t < 32 && c->aguess[c->t] >= 1.0) kg = ilogb(c->aguess[c->t]);   // previous probe, same t
+  else if (c->t > 0 && c->alpha_prev >= 1.0) kg = ilogb(c->alpha_prev);
   int k0 = kg - (MWU_MAXC / 2 - 1);
   if (k0 < 0) k0 = 0;
   int ks[MWU_MAXC];
@@ -349,6 +353,7 @@ __device__ void finalize(Ctl* c, int action, double* r) {
       set_cond(c->h_search, c->sactive ? 1u : 0u);
       break;
     case A_UPDATE: {
+      if (c->t < 32) c->ahist[c->t] = c->alpha;
       c->t++;
       c->alpha_last = c->alpha; c->alpha_prev = c->alpha; c->apply_prev = 1;
       if (c->pSing) { c->yS = c->yS + c->alpha * c->dyS; c->sP = c->yS; c->SP = 1.0; }
@@ -1226,33 +1231,42 @@ __device__ __forceinline__ void red_add_f64(double* p, double v) {
 // kernel reads x and d, and writes x, z and d, only for edges active in this or the last step.
 __device__ __forceinline__ bool act_bit(const uint32_t* act, int e) { return (__ldg(act + (e >> 5)) >> (e & 31)) & 1u; }
 
-// Software-pipelined over tiles: the streamed inputs of tile i+1 (z, src/dst rows, activity
-// word) and its u gathers are in flight while tile i is computed, so the DRAM latency of the
-// stream and the L2 latency of the gathers overlap the (exp / division heavy) arithmetic.
-struct ColIn {
-  double z[kColEdges];
-  int sr[kColEdges], dr[kColEdges];
-  uint32_t pw[kColEdges];
-};
+// The per-edge stream of each 512-edge tile (z, src/dst rows, activity words) is staged into
+// shared memory by the bulk-copy engine (cp.async.bulk + mbarrier) kColStages tiles ahead; the
+// u gathers of tile i+1 are issued (registers) before tile i is computed.  Stages are released per warp (an 8-arrival "empty" mbarrier), so
+// only the producer thread waits for the slowest warp; no block-wide barrier in the loop.
+constexpr int kColStages = 4;
+constexpr int kColOffS = MWU_CT * 8, kColOffD = kColOffS + MWU_CT * 4, kColOffA = kColOffD + MWU_CT * 4;
+constexpr int kColStageBytes = ((kColOffA + (MWU_CT / 32) * 4) + 127) / 128 * 128;
+constexpr size_t kColSmem = (size_t)kColStages * kColStageBytes;
 
-__device__ __forceinline__ void col_load(ColIn& in, int tile, int E, const double* __restrict__ z,
-                                         const int32_t* __restrict__ srow, const int32_t* __restrict__ drow,
-                                         const uint32_t* __restrict__ act) {
+__device__ __forceinline__ uint32_t r16(uint32_t b) { return (b + 15u) & ~15u; }
+
+__device__ __forceinline__ void col_issue(char* stage, uint64_t* bar, int tile, int E, const double* z,
+                                          const int32_t* srow, const int32_t* drow, const uint32_t* act) {
+  const int e0 = tile * MWU_CT;
+  const int rows = min(MWU_CT, E - e0);
+  const uint32_t bz = r16(rows * 8u), bi = r16(rows * 4u), ba = r16(((rows + 31) / 32) * 4u);
+  mbar_expect_tx(bar, bz + 2 * bi + ba);
+  tma_load_1d(stage, z + e0, bz, bar);
+  tma_load_1d(stage + kColOffS, srow + e0, bi, bar);
+  tma_load_1d(stage + kColOffD, drow + e0, bi, bar);
+  tma_load_1d(stage + kColOffA, act + (e0 >> 5), ba, bar);
+}
+
+// this thread's u gathers of a staged tile (registers; issued one tile ahead of their use)
+__device__ __forceinline__ void col_gather(const char* stage, int rows, const double* __restrict__ u, double* us,
+                                           double* ud) {
+  const int32_t* ssr = reinterpret_cast<const int32_t*>(stage + kColOffS);
+  const int32_t* sdr = reinterpret_cast<const int32_t*>(stage + kColOffD);
 #pragma unroll
   for (int k = 0; k < kColEdges; ++k) {
-    const int e = tile * MWU_CT + k * MWU_NT + threadIdx.x;
-    if (e < E) {
-      in.pw[k] = __ldg(act + (e >> 5));
-      in.z[k] = __ldcs(z + e);
-      in.sr[k] = __ldcs(srow + e);
-      in.dr[k] = __ldcs(drow + e);
-    } else {
-      in.pw[k] = 0u; in.z[k] = INFINITY; in.sr[k] = -1; in.dr[k] = -1;
-    }
+    const int j = k * MWU_NT + threadIdx.x;
+    if (j < rows) { us[k] = __ldg(u + ssr[j]); ud[k] = __ldg(u + sdr[j]); }
   }
 }
 
-__global__ void __launch_bounds__(MWU_NT, 3) col_densest_fast(
+__global__ void __launch_bounds__(MWU_NT, 2) col_densest_fast(
     int64_t E64, const int32_t* __restrict__ srow, const int32_t* __restrict__ drow, const double* __restrict__ u,
     double* __restrict__ x, double* __restrict__ d, double* __restrict__ z, double* __restrict__ dy,
     uint32_t* __restrict__ act, double* __restrict__ rz, double* __restrict__ rdz, double* __restrict__ rv,
@@ -1267,73 +1281,111 @@ __global__ void __launch_bounds__(MWU_NT, 3) col_densest_fast(
   double im = INFINITY, is = 0.0;          // inactive rows: min z and sum of v (shift s_C)
   double2* x2 = reinterpret_cast<double2*>(x);
   double2* d2 = reinterpret_cast<double2*>(d);
+  extern __shared__ __align__(128) char csm[];
+  __shared__ __align__(8) uint64_t full[kColStages], empty[kColStages];
   const int ntiles = (E + MWU_CT - 1) / MWU_CT;
-  int tile = blockIdx.x;
-  ColIn cur, nxt;
-  double us[kColEdges], ud[kColEdges];
-  if (tile < ntiles) {
-    col_load(cur, tile, E, z, srow, drow, act);
-#pragma unroll
-    for (int k = 0; k < kColEdges; ++k)
-      if (cur.sr[k] >= 0) { us[k] = __ldg(u + cur.sr[k]); ud[k] = __ldg(u + cur.dr[k]); }
+  const int mine = (ntiles > (int)blockIdx.x) ? (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kColStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], MWU_NT / 32); }
+    fence_barrier_init();
   }
-  for (; tile < ntiles; tile += gridDim.x) {
-    const int tn = tile + gridDim.x;
-    if (tn < ntiles) col_load(nxt, tn, E, z, srow, drow, act);    // next tile's stream, in flight
-    const int e0 = tile * MWU_CT + threadIdx.x;
-    int nact = 0;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int k = 0; k < mine && k < kColStages; ++k)
+      col_issue(csm + k * kColStageBytes, &full[k], blockIdx.x + k * gridDim.x, E, z, srow, drow, act);
+  double us[kColEdges], ud[kColEdges], nus[kColEdges], nud[kColEdges];
+  if (mine > 0) {
+    mbar_wait(&full[0], 0u);
+    col_gather(csm, min(MWU_CT, E - (int)blockIdx.x * MWU_CT), u, us, ud);
+  }
+  // double-buffered gather registers (no register moves that would wait on the loads)
+  auto body = [&](int kt, double (&us)[kColEdges], double (&ud)[kColEdges], double (&nus)[kColEdges],
+                  double (&nud)[kColEdges]) {
+    const int tile = blockIdx.x + kt * gridDim.x;
+    const int slot = kt % kColStages;
+    char* stg = csm + slot * kColStageBytes;
+    const int e0 = tile * MWU_CT;
+    const int rows = min(MWU_CT, E - e0);
+    // the next tile's gathers are in flight while this one is computed
+    if (kt + 1 < mine) {
+      const int ns = (kt + 1) % kColStages;
+      mbar_wait(&full[ns], (uint32_t)(((kt + 1) / kColStages) & 1));
+      col_gather(csm + ns * kColStageBytes, min(MWU_CT, E - (tile + (int)gridDim.x) * MWU_CT), u, nus, nud);
+    }
+    const double* sz = reinterpret_cast<const double*>(stg);
+    const int32_t* ssr = reinterpret_cast<const int32_t*>(stg + kColOffS);
+    const int32_t* sdr = reinterpret_cast<const int32_t*>(stg + kColOffD);
+    const uint32_t* sac = reinterpret_cast<const uint32_t*>(stg + kColOffA);
     double zk[kColEdges], dzk[kColEdges], vk[kColEdges];
+    double2 xe[kColEdges], dp[kColEdges];
+    bool had[kColEdges];
+    uint32_t pw[kColEdges];
+#pragma unroll
+    for (int k = 0; k < kColEdges; ++k) {                        // x, d of the previously active
+      const int j = k * MWU_NT + threadIdx.x;
+      pw[k] = j < rows ? sac[j >> 5] : 0u;
+      had[k] = (pw[k] >> lane) & 1u;
+      if (had[k]) { xe[k] = x2[e0 + j]; dp[k] = d2[e0 + j]; }
+    }
+    int nact = 0;
 #pragma unroll
     for (int k = 0; k < kColEdges; ++k) {
-      const int e = e0 + k * MWU_NT;
-      const bool had = (cur.pw[k] >> lane) & 1u;
-      double2 xe = make_double2(0.0, 0.0), dp = xe;
-      if (had) { xe = x2[e]; dp = d2[e]; }
-      double zz = cur.z[k];
+      const int j = k * MWU_NT + threadIdx.x;
+      const int e = e0 + j;
+      const bool valid = j < rows;
+      double zz = valid ? sz[j] : INFINITY;
+      const int sr = valid ? ssr[j] : -1, dr = valid ? sdr[j] : -1;
       double d0 = 0.0, d1 = 0.0, v = 0.0;
-      if (e < E) {
-        if (apply && had) {                                       // lazy x, z += alpha d
-          xe.x = xe.x + ap * dp.x;
-          xe.y = xe.y + ap * dp.y;
-          x2[e] = xe;
-          const double dzp = dp.x + dp.y;                         // d^(z)_e = (W d)_e of the last step
+      if (valid) {
+        if (apply && had[k]) {                                    // lazy x, z += alpha d
+          xe[k].x = xe[k].x + ap * dp[k].x;
+          xe[k].y = xe[k].y + ap * dp[k].y;
+          x2[e] = xe[k];
+          const double dzp = dp[k].x + dp[k].y;                   // d^(z)_e = (W d)_e of the last step
           zz = zz + ap * dzp;
           z[e] = zz;
         }
-        v = mwu_exp(neta * (zz - sC));                                // covering weight (Q4)
+#if MWU_ABLATE == 2
+        v = 1.0 + neta * (zz - sC);
+#else
+        v = mwu_exp(neta * (zz - sC));                            // covering weight (Q4)
+#endif
         const double h = v * rSC;                                 // W^T w_c
+#if MWU_ABLATE == 1
+        const double g0 = invD * (zz * rSP), g1 = invD * (zz * 0.5 * rSP);
+#else
         const double g0 = invD * (us[k] * rSP);                   // (1/D) O^T w_p
         const double g1 = invD * (ud[k] * rSP);
+#endif
         if (gdbg) { gdbg[2 * e] = g0; gdbg[2 * e + 1] = g1; hdbg[2 * e] = h; hdbg[2 * e + 1] = h; }
         // g >= h gives fl(g/h) >= 1, i.e. d = 0 exactly
         const bool a0 = g0 < h, a1 = g1 < h;
-        if ((a0 || a1) && !had) xe = x2[e];                       // newly active: fetch x
-        if (a0) d0 = mwu_direction(g0, h, xe.x, sigma);
-        if (a1) d1 = mwu_direction(g1, h, xe.y, sigma);
+        if ((a0 || a1) && !had[k]) xe[k] = x2[e];                 // newly active: fetch x
+        if (a0) d0 = mwu_direction(g0, h, xe[k].x, sigma);
+        if (a1) d1 = mwu_direction(g1, h, xe[k].y, sigma);
       }
       const double dz = d0 + d1;
       const bool nz = dz > 0.0;
       if (nz) { d2[e] = make_double2(d0, d1); ++nact; const double m01 = d0 > d1 ? d0 : d1; maxd = m01 > maxd ? m01 : maxd; }
-      else if (e < E) { im = zz < im ? zz : im; is += v; maxd = maxd > 0.0 ? maxd : 0.0; }   // candidate-independent row
+      else if (valid) { im = zz < im ? zz : im; is += v; maxd = maxd > 0.0 ? maxd : 0.0; }   // candidate-independent row
       zk[k] = zz; dzk[k] = dz; vk[k] = v;
       const uint32_t bw = __ballot_sync(0xffffffffu, nz);
-      if (lane == 0 && e < E && bw != cur.pw[k]) act[e >> 5] = bw;
-      if (d1 > 0.0) red_add_f64(dy + cur.dr[k], invD * d1);       // dst side: random rows
+      if (lane == 0 && valid && bw != pw[k]) act[e >> 5] = bw;
+#if MWU_ABLATE != 3
+      if (d1 > 0.0) red_add_f64(dy + dr, invD * d1);              // dst side: random rows
+#endif
       // src side: edges are sorted by src, so lanes of a warp hold runs of equal rows
       const double val = d0 > 0.0 ? invD * d0 : 0.0;
       if (__any_sync(0xffffffffu, val > 0.0)) {
         double run;
-        if (warp_run_sum(cur.sr[k], val, run) && run > 0.0) red_add_f64(dy + cur.sr[k], run);
+        if (warp_run_sum(sr, val, run) && run > 0.0) red_add_f64(dy + sr, run);
       }
     }
-    // the next tile's gathers (its src/dst rows have arrived by now)
-    if (tn < ntiles) {
-#pragma unroll
-      for (int k = 0; k < kColEdges; ++k)
-        if (nxt.sr[k] >= 0) { us[k] = __ldg(u + nxt.sr[k]); ud[k] = __ldg(u + nxt.dr[k]); }
-    }
+    // this warp is done with the stage: release it
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
     // compaction of the active covering rows: each warp owns the record segment
-    // [tile*CT + warp*kWarpSeg, +kWarpSeg) of its kWarpSeg edges (no block barrier)
+    // [tile*CT + warp*kWarpSeg, +kWarpSeg) of its kWarpSeg edges
     int incl = nact;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -1345,7 +1397,15 @@ __global__ void __launch_bounds__(MWU_NT, 3) col_densest_fast(
     for (int k = 0; k < kColEdges; ++k)
       if (dzk[k] > 0.0) { rz[p] = zk[k]; rdz[p] = dzk[k]; rv[p] = vk[k]; ++p; }
     if (lane == 31) tcnt[tile * (MWU_NT / 32) + warp] = incl;
-    cur = nxt;
+    if (threadIdx.x == 0 && kt + kColStages < mine) {           // producer: refill once all warps left
+      mbar_wait(&empty[slot], (uint32_t)((kt / kColStages) & 1));
+      col_issue(stg, &full[slot], blockIdx.x + (kt + kColStages) * gridDim.x, E, z, srow, drow, act);
+    }
+  };
+  for (int kt = 0; kt < mine; ++kt) {
+    body(kt, us, ud, nus, nud);
+#pragma unroll
+    for (int q = 0; q < kColEdges; ++q) { us[q] = nus[q]; ud[q] = nud[q]; }
   }
   double acc[3] = {maxd, im, is};
   const int ops[3] = {OP_MAX, OP_MIN, OP_SUM};

@@ -102,6 +102,7 @@ struct mwu_ctx {
   int sms = 148, grid_rows = 592, grid_max = 1184;
   std::vector<void*> allocs;
   bool probe_active = false;
+  double aguess[32] = {0};   // accepted step sizes of the last probe by iteration (first-window guess)
   double bound = 0, eps = 0;
   int record = 0;
   cudaGraph_t graph = nullptr;
@@ -318,6 +319,7 @@ void init_ctx_common(mwu_ctx* c, const mwu_options* opt) {
   c->part = dalloc<double>(c, (int64_t)c->grid_max * MWU_SLOTS);
   c->counter = dalloc<unsigned int>(c, 1);
   CK(cudaFuncSetAttribute(search_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSearchSmem));
+  CK(cudaFuncSetAttribute(col_densest_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kColSmem));
   CK(cudaMemsetAsync(c->counter, 0, sizeof(unsigned int), c->st));
   CK(cudaEventCreate(&c->ev0));
   CK(cudaEventCreate(&c->ev1));
@@ -456,9 +458,12 @@ void build_graph_storage(mwu_ctx* c, const mwu_graph* g) {
 }
 
 // ------------------------------------------------------------------------------ multi-GPU
+// contiguous ranges on MWU_CT-edge tile boundaries (keeps the sliced per-edge arrays 16-byte
+// aligned for the bulk copies and the activity words whole)
 void shard_range(int64_t n, int world, int rank, int64_t& a, int64_t& b) {
-  a = (int64_t)((__int128)n * rank / world);
-  b = (int64_t)((__int128)n * (rank + 1) / world);
+  const int64_t tiles = (n + MWU_CT - 1) / MWU_CT;
+  a = std::min(n, (int64_t)((__int128)tiles * rank / world) * MWU_CT);
+  b = (rank + 1 == world) ? n : std::min(n, (int64_t)((__int128)tiles * (rank + 1) / world) * MWU_CT);
 }
 
 // complete a deferred partial reduction: gather every rank's slots, combine in rank order
@@ -656,8 +661,8 @@ void enqueue_column(mwu_ctx* c, cudaStream_t st) {
       if (c->lazyC) {
         CK(cudaMemsetAsync(c->dy, 0, (c->mP > 0 ? c->mP : 1) * sizeof(double), st));
         const int64_t nt = c->ntilesC;
-        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(nt, 3 * c->sms));
-        col_densest_fast<<<g, MWU_NT, 0, st>>>(c->E, c->srow, c->drow, c->u, c->x, c->d, c->z, c->dy, c->act, c->rz,
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(nt, 2 * c->sms));
+        col_densest_fast<<<g, MWU_NT, kColSmem, st>>>(c->E, c->srow, c->drow, c->u, c->x, c->d, c->z, c->dy, c->act, c->rz,
                                               c->rdz, c->rv, c->tcnt, c->record ? c->gdbg : nullptr,
                                               c->record ? c->hdbg : nullptr, c->ctl, c->part, c->counter);
         inactive_exact<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, c->act, c->z, c->ctl, c->part, c->counter);
@@ -854,6 +859,7 @@ void probe_begin(mwu_ctx* c, double bound, double eps) {
   h.use_graph = c->opt.use_graph;
   h.lazyC = c->lazyC;
   h.world = c->world;
+  for (int i = 0; i < 32; ++i) h.aguess[i] = c->aguess[i];
   h.status = c->empty_cover ? ST_INFEASIBLE : ST_RUNNING;
   h.reason = c->empty_cover ? R_EMPTY_COVER : R_NONE;
   h.record = c->record;
@@ -949,6 +955,7 @@ float run_loop(mwu_ctx* c, int64_t k) {
   }
   pull_ctl(c);
   if (c->hctl->nan_flag) throw MwuError{MWU_ERR_NUMERIC, "non-finite weight sums"};
+  for (int i = 0; i < 32 && i < c->hctl->t; ++i) c->aguess[i] = c->hctl->ahist[i];
   return ms;
 }
 

@@ -11,7 +11,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libmwu.so")
+_SO = os.environ.get("MWU_SO") or os.path.join(_HERE, "libmwu.so")   # MWU_SO: ablation builds
 
 OK, ERR_ARG, ERR_CUDA, ERR_OOM, ERR_NCCL, ERR_STATE, ERR_NUMERIC = range(7)
 RUNNING, FEASIBLE, INFEASIBLE, ITER_LIMIT = range(4)
