@@ -1480,6 +1480,95 @@ __global__ void scatter_init(int64_t E, const int32_t* __restrict__ srow, const 
   }
 }
 
+// =====================================================================================
+// Fast transposed / forward products of the pure covering kinds (vcover c2, domset c3)
+// =====================================================================================
+// VCOVER (C = M^T): hs_v += v_e for both endpoints of every edge (h = M w_c), the src
+// side as warp-segmented runs of the sorted edge list, the dst side one fp64 reduction per edge
+// into the (L2-resident) vertex vector.
+__global__ void __launch_bounds__(MWU_NT) vc_scatter(int64_t E, const int32_t* __restrict__ src,
+                                                     const int32_t* __restrict__ dst, const double* __restrict__ v,
+                                                     double* __restrict__ hs, const Ctl* c) {
+  if (c->status != ST_RUNNING) return;
+  constexpr int U = 4;
+  const int64_t chunk = (int64_t)U * MWU_NT;
+  for (int64_t base = (int64_t)blockIdx.x * chunk; base < E; base += (int64_t)gridDim.x * chunk) {
+    double val[U];
+    int sr[U], dr[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t e = base + k * MWU_NT + threadIdx.x;
+      if (e < E) { val[k] = __ldcs(v + e); sr[k] = __ldcs(src + e); dr[k] = __ldcs(dst + e); }
+      else { val[k] = 0.0; sr[k] = -1; dr[k] = -1; }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      if (dr[k] >= 0) red_add_f64(hs + dr[k], val[k]);
+      double run;
+      if (warp_run_sum(sr[k], val[k], run) && sr[k] >= 0) red_add_f64(hs + sr[k], run);
+    }
+  }
+}
+
+// CSR rows sorted (row id per nonzero): out_r += w[col_k] (all values 1.0: C = I + A)
+__global__ void __launch_bounds__(MWU_NT) csr_scatter(int64_t nnz, const int32_t* __restrict__ rowid,
+                                                      const uint32_t* __restrict__ col, const double* __restrict__ w,
+                                                      double* __restrict__ out, const Ctl* c) {
+  if (c->status != ST_RUNNING) return;
+  constexpr int U = 4;
+  const int64_t chunk = (int64_t)U * MWU_NT;
+  for (int64_t base = (int64_t)blockIdx.x * chunk; base < nnz; base += (int64_t)gridDim.x * chunk) {
+    int r[U];
+    uint32_t cl[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t q = base + k * MWU_NT + threadIdx.x;
+      if (q < nnz) { r[k] = __ldcs(rowid + q); cl[k] = __ldcs(col + q); } else { r[k] = -1; cl[k] = 0; }
+    }
+    double val[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) val[k] = r[k] >= 0 ? __ldg(w + cl[k]) : 0.0;
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      double run;
+      if (warp_run_sum(r[k], val[k], run) && r[k] >= 0) red_add_f64(out + r[k], run);
+    }
+  }
+}
+
+// Column epilogue over the variables (pure covering, P = (1/M) 1^T): lazy x += alpha d,
+// h = (C^T v)_i / S_C, g = 1/M, d; reduces max d and sum(d)/M.
+__global__ void __launch_bounds__(MWU_NT) col_vertex(int64_t n, const double* __restrict__ hs, double* __restrict__ x,
+                                                     double* __restrict__ d, double* gdbg, double* hdbg, Ctl* c,
+                                                     double* part, unsigned int* counter) {
+  if (c->status != ST_RUNNING) return;
+  const double SC = c->SC, g = c->invB, sigma = c->sigma, ap = c->alpha_prev, invB = c->invB;
+  const int apply = c->apply_prev;
+  double acc[2] = {-INFINITY, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * MWU_NT) {
+    double xi = x[i];
+    const double dp = d[i];
+    if (apply && dp != 0.0) { xi = xi + ap * dp; x[i] = xi; }
+    const double h = hs[i] / SC;
+    const double di = (g < h) ? mwu_direction(g, h, xi, sigma) : 0.0;
+    if (di != dp) d[i] = di;
+    if (gdbg) { gdbg[i] = g; hdbg[i] = h; }
+    acc[0] = fmax(acc[0], di);
+    acc[1] += invB * di;
+  }
+  const int ops[2] = {OP_MAX, OP_SUM};
+  reduce_and_finalize<2>(acc, ops, part, counter, c, A_COL);
+}
+
+// Forward product done (scattered): set up the step search.
+__global__ void step_done(Ctl* c) {
+  if (threadIdx.x != 0) return;
+  if (c->status != ST_RUNNING) { set_cond(c->h_search, 0u); return; }
+  double r[MWU_SLOTS];
+  for (int s = 0; s < MWU_SLOTS; ++s) r[s] = 0.0;
+  finalize(c, A_STEP_DONE, r);
+}
+
 // Rare path of the inactive-row aggregate: when min_inactive z - s_C exceeds 600/eta the sum of
 // v at shift s_C may have lost terms to underflow; recompute it at shift mzi exactly.
 __global__ void __launch_bounds__(MWU_NT) inactive_exact(int64_t E, const uint32_t* __restrict__ act,

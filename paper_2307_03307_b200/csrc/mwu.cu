@@ -79,6 +79,9 @@ struct mwu_ctx {
   int lazyC = 0;
   int scatterP = 0;          // graph kinds with edge variables: d^(y) scattered by the column kernel
   uint32_t* perm = nullptr;  // scatterP: internal (L2-blocked) edge position -> original edge id
+  int fastC = 0;             // vcover / domset: transposed (and domset forward) products scattered
+  double* hsum = nullptr;    // fastC: C^T v per variable
+  int32_t* rowidC = nullptr; // fastC domset: row id of every nonzero of C = I + A
   // multi-GPU (edge-sharded): this rank owns internal edges [e0, e0 + E)
   int world = 1, rank = 0;
   Comm* comm = nullptr;
@@ -285,6 +288,7 @@ void alloc_vectors(mwu_ctx* c) {
   if (c->mC > mx) mx = c->mC;
   c->tmp = dalloc<double>(c, mx);
   if (c->scatterP) c->tmp2 = dalloc<double>(c, c->ng > 0 ? c->ng : c->n);
+  if (c->fastC) c->hsum = dalloc<double>(c, c->n);
   if (c->kind == K_CSR && !c->pSing && !c->cSing) c->gtmp = dalloc<double>(c, c->n);
   CK(cudaMemsetAsync(c->d, 0, c->n * sizeof(double), c->st));
   CK(cudaMemsetAsync(c->x, 0, c->n * sizeof(double), c->st));
@@ -675,10 +679,24 @@ void enqueue_column(mwu_ctx* c, cudaStream_t st) {
       c->launches++;
       break;
     case K_VCOVER:
-      launch_seg(c, st, c->inc_all, item_of(c->inc_all, c->v, 1, nullptr), make_col(c, 1, nullptr), A_COL);
-      break;
     case K_DOMSET:
-      launch_seg(c, st, c->cscC, item_of(c->cscC, c->v, 0, nullptr), make_col(c, 1, nullptr), A_COL);
+      if (c->fastC) {
+        CK(cudaMemsetAsync(c->hsum, 0, c->n * sizeof(double), st));
+        if (c->kind == K_VCOVER)
+          vc_scatter<<<(int)std::min<int64_t>(4 * c->sms, (c->E + 4 * MWU_NT - 1) / (4 * MWU_NT) + 1), MWU_NT, 0, st>>>(
+              c->E, c->src, c->dst, c->v, c->hsum, c->ctl);
+        else
+          csr_scatter<<<(int)std::min<int64_t>(4 * c->sms, (c->nnzC + 4 * MWU_NT - 1) / (4 * MWU_NT) + 1), MWU_NT, 0, st>>>(
+              c->nnzC, c->rowidC, c->csrC.idx, c->v, c->hsum, c->ctl);
+        col_vertex<<<rows_grid(c, c->n), MWU_NT, 0, st>>>(c->n, c->hsum, c->x, c->d, c->record ? c->gdbg : nullptr,
+                                                        c->record ? c->hdbg : nullptr, c->ctl, c->part, c->counter);
+        c->launches += 2;
+        break;
+      }
+      if (c->kind == K_VCOVER)
+        launch_seg(c, st, c->inc_all, item_of(c->inc_all, c->v, 1, nullptr), make_col(c, 1, nullptr), A_COL);
+      else
+        launch_seg(c, st, c->cscC, item_of(c->cscC, c->v, 0, nullptr), make_col(c, 1, nullptr), A_COL);
       break;
     case K_CSR:
       if (!c->pSing && !c->cSing) {
@@ -739,6 +757,14 @@ void enqueue_forward(mwu_ctx* c, cudaStream_t st, const double* in, double* oy, 
       c->launches++;
       break;
     case K_DOMSET:
+      if (c->fastC) {
+        CK(cudaMemsetAsync(oz, 0, c->mC * sizeof(double), st));
+        csr_scatter<<<(int)std::min<int64_t>(4 * c->sms, (c->nnzC + 4 * MWU_NT - 1) / (4 * MWU_NT) + 1), MWU_NT, 0, st>>>(
+            c->nnzC, c->rowidC, c->csrC.idx, in, oz, c->ctl);
+        c->launches++;
+        if (!init) { step_done<<<1, 32, 0, st>>>(c->ctl); c->launches++; }
+        break;
+      }
       launch_seg(c, st, c->csrC, item_of(c->csrC, in, 0, nullptr), ez, a_done);
       break;
     case K_CSR:
@@ -1250,9 +1276,16 @@ mwu_status mwu_create_graph(const mwu_graph* g, const mwu_options* opt, mwu_ctx*
         if (g->n_edges == 0) throw MwuError{MWU_ERR_ARG, "vertex cover needs at least one edge"};
         c->kind = K_VCOVER; c->mode = MWU_PURE_COVERING; c->n = c->nv; c->mC = c->E; c->pSing = 1;
         c->nnzC = 2 * c->E; c->nnzP = c->nv;
+        c->fastC = c->opt.deterministic ? 0 : 1;
         break;
       case MWU_G_DOMSET:
         c->kind = K_DOMSET; c->mode = MWU_PURE_COVERING; c->n = c->nv; c->mC = c->nv; c->pSing = 1; c->nnzP = c->nv;
+        c->fastC = c->opt.deterministic ? 0 : 1;
+        if (c->fastC && c->nnzC > 0) {
+          c->rowidC = dalloc<int32_t>(c, c->nnzC);
+          k_row_ids<<<grid_for(c, c->nv), MWU_NT, 0, c->st>>>(c->nv, c->csrC.rowptr, (uint32_t*)c->rowidC);
+          CKL();
+        }
         break;
       case MWU_G_DENSEST:
         if (g->n_edges == 0) throw MwuError{MWU_ERR_ARG, "densest subgraph needs at least one edge"};

@@ -230,6 +230,19 @@ def test_graph_and_host_modes_bit_identical(cuda_ok):
     assert torch.equal(a.x(), b.x())
 
 
+@pytest.mark.parametrize("kind", ["vcover", "domset", "bmatch"])
+def test_deterministic_path_parity(cuda_ok, kind):
+    """The fixed-order (deterministic=1) engine of the other graph kinds under the same lockstep
+    checks as the default scattered path."""
+    G = _graph(kind, 0)
+    s, d = G.numpy()
+    B, _ = _oracle_probe_bound(kind, G)
+    lp = O.graph_lp(kind, s, d, G.n_vertices, B)
+    probe = O.Probe(lp, EPS[kind], max_iter=5000)
+    S = solver_for(kind, G, deterministic=1)
+    lockstep(S, probe, B, EPS[kind], 50, alphas=None, window=self_sensitivity_window(lp, EPS[kind], None, 50))
+
+
 @pytest.mark.parametrize("i", [0, 1])
 def test_densest_deterministic_path_parity(cuda_ok, i):
     """The fixed-order densest path (deterministic=1: stored v and d^(z), gathered forward
@@ -258,10 +271,12 @@ def test_densest_fast_path_repeatable_objective(cuda_ok):
 
 
 def test_bisect_depth_does_not_change_results(cuda_ok):
+    """How many bisection levels a search pass evaluates changes only the pass count, never
+    Alg. 3's result (deterministic=1: fixed-order sums, so the comparison is bit-exact)."""
     G = gg.erdos_renyi(3000, 20000, seed=10)
     xs, its = [], []
     for depth in (1, 2, 3):
-        S = solver_for("vcover", G, bisect_depth=depth)
+        S = solver_for("vcover", G, bisect_depth=depth, deterministic=1)
         S.solve(0.05, 500)
         xs.append(S.x())
         its.append(S.stats()["iters_total"])
