@@ -32,7 +32,7 @@ def test_shard_ranges_tile_the_edges(E, W):
         sizes.append(b - a)
         prev = b
     assert prev == E
-    assert max(sizes) - min(sizes) <= 512 + 1          # ranges on 512-edge tile boundaries
+    assert max(sizes) - min(sizes) <= 2 * 1024          # ranges on MWU_CT = 1024-edge tile boundaries
 
 
 def _free_port():
