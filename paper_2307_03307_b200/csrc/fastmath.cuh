@@ -95,6 +95,72 @@ MWU_HD void mwu_expm1_exp(double x, double& em, double& q) {
   }
 }
 
+// exp(x) from a 256-entry table T[j] = 2^(j/256) (host-filled by mwu_exp_table, kept by the
+// caller in shared memory) and a degree-5 polynomial on |r| <= ln2/512: half the dependent FMA
+// chain of mwu_expm1_exp (the column kernel is bound by that latency).
+MWU_HD void mwu_exp_table(double* T) {
+  for (int j = 0; j < 256; ++j) T[j] = exp2((double)j / 256.0);
+}
+// host: T[i] = 2^((i-128)/256) and T[i] - 1 as an unevaluated hi + lo pair (long double)
+inline void mwu_expm1_tables(double* T, double* Mh, double* Ml) {
+  for (int i = 0; i < 256; ++i) {
+    const int j = i - 128;
+    const long double t = exp2l((long double)j / 256.0L);
+    T[i] = (double)t;
+    const long double m = t - 1.0L;
+    Mh[i] = (double)m;
+    Ml[i] = (double)(m - (long double)Mh[i]);
+  }
+}
+
+// (expm1(x), exp(x)) from the 256-entry tables (T, T - 1 as hi + lo; j in [-128, 128), so
+// |x| < ln2/2 needs no 2^k scaling and expm1 suffers no cancellation) and a degree-5
+// polynomial: both accurate relative to themselves, with half the dependent FMA chain of
+// mwu_expm1_exp.
+MWU_HD void mwu_expm1_exp_tab(double x, const double* T, const double* Mh, const double* Ml, double& em, double& q) {
+  if (!(x >= -745.5)) { em = -1.0; q = 0.0; return; }
+  if (x > 709.78) { em = INFINITY; q = INFINITY; return; }
+  const double kd = rint(x * 369.3299304675746);              // 256 / ln2
+  double r = MWU_FMA(-kd, 0.00270760617331689, x);             // ln2/256 hi, 32 bits (exact product)
+  r = MWU_FMA(-kd, 7.453964567463233e-13, r);                  // ln2/256 lo
+  const int ki = (int)kd;
+  const int i = ((ki + 128) & 255), k = (ki - (i - 128)) / 256;   // kd = 256 k + (i - 128)
+  double p = 1.0 / 120.0;
+  p = MWU_FMA(p, r, 1.0 / 24.0);
+  p = MWU_FMA(p, r, 1.0 / 6.0);
+  p = MWU_FMA(p, r, 0.5);
+  p = MWU_FMA(p, r * r, r);                                    // expm1(r)
+  const double t = T[i];
+  const double tp = t * p;
+  const double e0 = Mh[i] + (tp + Ml[i]);                      // 2^(j/256) e^r - 1
+  if (k >= -1021) {
+    const double s = mwu_pow2i(k);
+    q = MWU_FMA(t, p, t) * s;
+    em = (k == 0) ? e0 : MWU_FMA(s, e0, s - 1.0);
+  } else {
+    q = (MWU_FMA(t, p, t) * mwu_pow2i(k + 60)) * 8.673617379884035e-19;
+    em = -1.0;
+  }
+}
+MWU_HD double mwu_exp_tab(double x, const double* T) {
+  if (!(x >= -745.5)) return 0.0;
+  if (x > 709.78) return INFINITY;
+  const double kd = rint(x * 369.3299304675746);              // 256 / ln2
+  double r = MWU_FMA(-kd, 0.00270760617331689, x);             // ln2/256 hi, 32 bits (exact product)
+  r = MWU_FMA(-kd, 7.453964567463233e-13, r);                 // ln2/256 lo
+  const int ki = (int)kd;
+  const int j = ki & 255, k = (ki - j) / 256;                  // kd = 256 k + j, 0 <= j < 256
+  double p = 1.0 / 120.0;
+  p = MWU_FMA(p, r, 1.0 / 24.0);
+  p = MWU_FMA(p, r, 1.0 / 6.0);
+  p = MWU_FMA(p, r, 0.5);
+  p = MWU_FMA(p, r * r, r);                                    // expm1(r)
+  const double t = T[j];
+  const double m = MWU_FMA(t, p, t);                           // 2^(j/256) e^r
+  if (k >= -1021) return m * mwu_pow2i(k);
+  return (m * mwu_pow2i(k + 60)) * 8.673617379884035e-19;
+}
+
 MWU_HD double mwu_exp(double x) {
   double em, q;
   mwu_expm1_exp(x, em, q);

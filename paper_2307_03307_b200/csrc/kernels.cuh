@@ -798,7 +798,9 @@ struct PRowFast {
   double ep[NC], mx[NC];
   double shP[NC];
   bool lse[NC];        // Q16: candidates with eta alpha max d^(y) > 700 use the shifted exp sum
-  __device__ PRowFast(const Cands& k, double e) : ea0(k.ea0), ead(k.ead), eta(e) {
+  const double *T, *Mh, *Ml;   // exp tables (shared memory)
+  __device__ PRowFast(const Cands& k, double e, const double* tab) : ea0(k.ea0), ead(k.ead), eta(e),
+                                                                      T(tab), Mh(tab + 256), Ml(tab + 512) {
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
       a[j] = k.a[j]; sq[j] = k.sq[j]; ep[j] = 0.0; mx[j] = -INFINITY; shP[j] = k.shP[j]; lse[j] = (k.mP[j] == CM_LSE);
@@ -834,7 +836,8 @@ struct CRowFast {
   double a[NC], ea0, ead;
   int sq[NC];
   double ec[NC], tc[NC], mn[NC];
-  __device__ CRowFast(const Cands& k) : ea0(k.ea0), ead(k.ead) {
+  const double *T, *Mh, *Ml;   // exp tables (shared memory)
+  __device__ CRowFast(const Cands& k, const double* tab) : ea0(k.ea0), ead(k.ead), T(tab), Mh(tab + 256), Ml(tab + 512) {
 #pragma unroll
     for (int j = 0; j < NC; ++j) { a[j] = k.a[j]; sq[j] = k.sq[j]; ec[j] = 0.0; tc[j] = 0.0; mn[j] = INFINITY; }
   }
@@ -1000,25 +1003,26 @@ struct SearchArgs {
   int64_t mP; const double *y, *dy, *u;                  // this rank's slice of the packing rows
   int64_t mC; const double *z, *dz, *v;                  // dense covering rows (v: weights)
   const double *rz, *rdz, *rv; const int32_t* tcnt; int64_t ntiles;   // compacted (rz != nullptr)
+  const double* emtab;                                   // 768: T, T-1 hi, T-1 lo (fastmath.cuh)
 };
 
 template <int PT, int NC, bool SQ1>
 __device__ __forceinline__ void search_body_fast(const SearchArgs& A, const Cands& K, const Ctl* c, double* sbuf,
-                                                 uint64_t* bars, double* part) {
+                                                 uint64_t* bars, double* part, const double* tab) {
   uint32_t it = 0;
   const int opsS[NC] = {};   // all OP_SUM (0)
   int opsX[NC], opsN[NC];
 #pragma unroll
   for (int j = 0; j < NC; ++j) { opsX[j] = OP_MAX; opsN[j] = OP_MIN; }
   {
-    PRowFast<PT, NC, SQ1> f(K, c->eta);
+    PRowFast<PT, NC, SQ1> f(K, c->eta, tab);
     if (!c->pSing) stream_rows3(A.y, A.dy, A.u, A.mP, sbuf, bars, it, f);
     block_partials<NC>(f.ep, opsS, part, R_EP(0));
     block_partials<NC>(f.ep, opsS, part, R_LP(0));          // LSE-mode candidates read this slot
     block_partials<NC>(f.mx, opsX, part, R_MX(0));
   }
   {
-    CRowFast<PT, NC, SQ1> f(K);
+    CRowFast<PT, NC, SQ1> f(K, tab);
     if (!c->cSing) {
       if (A.rz) for_compact_rows(A.rz, A.rdz, A.rv, A.tcnt, A.ntiles, f);
       else stream_rows3(A.z, A.dz, A.v, A.mC, sbuf, bars, it, f);
@@ -1078,6 +1082,8 @@ __global__ void __launch_bounds__(MWU_NT, 2) search_pass(SearchArgs A, Ctl* c, d
   }
   extern __shared__ __align__(128) double sbuf[];
   __shared__ __align__(8) uint64_t bars[MWU_SST];
+  __shared__ double s_tab[768];
+  for (int i = threadIdx.x; i < 768; i += MWU_NT) s_tab[i] = A.emtab[i];
   if (threadIdx.x == 0) {
     for (int s = 0; s < MWU_SST; ++s) mbar_init(&bars[s], 1);
     fence_barrier_init();
@@ -1085,7 +1091,7 @@ __global__ void __launch_bounds__(MWU_NT, 2) search_pass(SearchArgs A, Ctl* c, d
   __syncthreads();
   if (fast) {
 #define MWU_FAST_CASE(PTV, N, S) \
-    if (K.pt == PTV && K.nc == N && sq1 == S) search_body_fast<PTV, N, S>(A, K, c, sbuf, bars, part); else
+    if (K.pt == PTV && K.nc == N && sq1 == S) search_body_fast<PTV, N, S>(A, K, c, sbuf, bars, part, s_tab); else
     MWU_FAST_CASE(PT_DOUBLE, 8, true) MWU_FAST_CASE(PT_DOUBLE, 7, true) MWU_FAST_CASE(PT_DOUBLE, 6, true)
     MWU_FAST_CASE(PT_DOUBLE, 5, true) MWU_FAST_CASE(PT_DOUBLE, 4, true) MWU_FAST_CASE(PT_DOUBLE, 3, true)
     MWU_FAST_CASE(PT_DOUBLE, 2, true) MWU_FAST_CASE(PT_DOUBLE, 1, true)
@@ -1248,9 +1254,10 @@ __device__ __forceinline__ void col_issue(char* stage, uint64_t* bar, int tile, 
   const int rows = min(MWU_CT, E - e0);
   const uint32_t bz = r16(rows * 8u), bi = r16(rows * 4u), ba = r16(((rows + 31) / 32) * 4u);
   mbar_expect_tx(bar, bz + 2 * bi + ba);
-  tma_load_1d(stage, z + e0, bz, bar);
-  tma_load_1d(stage + kColOffS, srow + e0, bi, bar);
-  tma_load_1d(stage + kColOffD, drow + e0, bi, bar);
+  const uint64_t pf = pol_first();
+  tma_load_1d_hint(stage, z + e0, bz, bar, pf);
+  tma_load_1d_hint(stage + kColOffS, srow + e0, bi, bar, pf);
+  tma_load_1d_hint(stage + kColOffD, drow + e0, bi, bar, pf);
   tma_load_1d(stage + kColOffA, act + (e0 >> 5), ba, bar);
 }
 
@@ -1270,8 +1277,11 @@ __global__ void __launch_bounds__(MWU_NT, 2) col_densest_fast(
     int64_t E64, const int32_t* __restrict__ srow, const int32_t* __restrict__ drow, const double* __restrict__ u,
     double* __restrict__ x, double* __restrict__ d, double* __restrict__ z, double* __restrict__ dy,
     uint32_t* __restrict__ act, double* __restrict__ rz, double* __restrict__ rdz, double* __restrict__ rv,
-    int32_t* __restrict__ tcnt, double* gdbg, double* hdbg, Ctl* c, double* part, unsigned int* counter) {
+    int32_t* __restrict__ tcnt, double* gdbg, double* hdbg, Ctl* c, double* part, unsigned int* counter,
+    const double* __restrict__ exptab) {
   if (c->status != ST_RUNNING) return;
+  __shared__ double s_tab[256];                                   // 2^(j/256), host-rounded
+  s_tab[threadIdx.x] = exptab[threadIdx.x];                       // MWU_NT == 256
   const double rSP = 1.0 / c->SP, rSC = 1.0 / c->SC, invD = c->invB, sigma = c->sigma, ap = c->alpha_prev;
   const double neta = -c->eta, sC = c->sC;
   const int apply = c->apply_prev;
@@ -1348,7 +1358,7 @@ __global__ void __launch_bounds__(MWU_NT, 2) col_densest_fast(
 #if MWU_ABLATE == 2
         v = 1.0 + neta * (zz - sC);
 #else
-        v = mwu_exp(neta * (zz - sC));                            // covering weight (Q4)
+        v = mwu_exp_tab(neta * (zz - sC), s_tab);                 // covering weight (Q4)
 #endif
         const double h = v * rSC;                                 // W^T w_c
 #if MWU_ABLATE == 1

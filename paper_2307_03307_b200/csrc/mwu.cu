@@ -80,6 +80,8 @@ struct mwu_ctx {
   int scatterP = 0;          // graph kinds with edge variables: d^(y) scattered by the column kernel
   uint32_t* perm = nullptr;  // scatterP: internal (L2-blocked) edge position -> original edge id
   int fastC = 0;             // vcover / domset: transposed (and domset forward) products scattered
+  double* exptab = nullptr;  // 2^(j/256), j < 256 (fastmath.cuh mwu_exp_tab)
+  double* emtab = nullptr;   // 2^(j/256), j in [-128, 128), and 2^(j/256) - 1 as hi + lo
   double* hsum = nullptr;    // fastC: C^T v per variable
   int32_t* rowidC = nullptr; // fastC domset: row id of every nonzero of C = I + A
   // multi-GPU (edge-sharded): this rank owns internal edges [e0, e0 + E)
@@ -322,6 +324,16 @@ void init_ctx_common(mwu_ctx* c, const mwu_options* opt) {
   CK(cudaMemsetAsync(c->ctl, 0, sizeof(Ctl), c->st));
   c->part = dalloc<double>(c, (int64_t)c->grid_max * MWU_SLOTS);
   c->counter = dalloc<unsigned int>(c, 1);
+  {
+    double T[256];
+    mwu_exp_table(T);
+    c->exptab = dalloc<double>(c, 256);
+    CK(cudaMemcpy(c->exptab, T, sizeof(T), cudaMemcpyHostToDevice));
+    double E3[768];
+    mwu_expm1_tables(E3, E3 + 256, E3 + 512);
+    c->emtab = dalloc<double>(c, 768);
+    CK(cudaMemcpy(c->emtab, E3, sizeof(E3), cudaMemcpyHostToDevice));
+  }
   CK(cudaFuncSetAttribute(search_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSearchSmem));
   CK(cudaFuncSetAttribute(col_densest_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kColSmem));
   CK(cudaMemsetAsync(c->counter, 0, sizeof(unsigned int), c->st));
@@ -668,7 +680,7 @@ void enqueue_column(mwu_ctx* c, cudaStream_t st) {
         const int g = (int)std::max<int64_t>(1, std::min<int64_t>(nt, 2 * c->sms));
         col_densest_fast<<<g, MWU_NT, kColSmem, st>>>(c->E, c->srow, c->drow, c->u, c->x, c->d, c->z, c->dy, c->act, c->rz,
                                               c->rdz, c->rv, c->tcnt, c->record ? c->gdbg : nullptr,
-                                              c->record ? c->hdbg : nullptr, c->ctl, c->part, c->counter);
+                                              c->record ? c->hdbg : nullptr, c->ctl, c->part, c->counter, c->exptab);
         inactive_exact<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, c->act, c->z, c->ctl, c->part, c->counter);
         c->launches += 2;
         break;
@@ -793,6 +805,7 @@ void enqueue_search(mwu_ctx* c, cudaStream_t st) {
   A.mP = p1 - p0; A.y = c->y + p0; A.dy = c->dy + p0; A.u = c->u + p0;
   A.mC = c->mC; A.z = c->z; A.dz = c->dz; A.v = c->v;
   A.rz = c->rz; A.rdz = c->rdz; A.rv = c->rv; A.tcnt = c->tcnt; A.ntiles = c->ntilesC;
+  A.emtab = c->emtab;
   search_pass<<<g, MWU_NT, kSearchSmem, st>>>(A, c->ctl, c->part, c->counter);
   c->launches++;
 }

@@ -52,6 +52,53 @@ def test_exp_expm1_accuracy(fm):
     assert worst_q <= 4 and worst_em <= 4, (worst_q, worst_em)
 
 
+def test_table_exp_accuracy(tmp_path):
+    so = str(tmp_path / "fm2.so")
+    subprocess.run(["g++", "-O2", "-ffp-contract=off", "-shared", "-fPIC", "-o", so,
+                    os.path.join(ROOT, "tests", "native", "fastmath_host.cpp")], check=True)
+    L = ctypes.CDLL(so)
+    L.fm_exp_tab.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_long]
+    mpmath.mp.dps = 50
+    rng = np.random.default_rng(11)
+    xs = np.concatenate([rng.uniform(-745, 0, 3000), rng.uniform(-2, 2, 2000), rng.uniform(0, 709, 500),
+                         [0.0, -1e-300, 1e-12, -0.0013538, 709.7, -745.1]])
+    q = np.empty_like(xs)
+    L.fm_exp_tab(xs.ctypes.data, q.ctypes.data, xs.size)
+    worst = 0.0
+    for x, b in zip(xs, q):
+        e = float(mpmath.exp(mpmath.mpf(x)))
+        if e >= 2.2250738585072014e-308:
+            worst = max(worst, _ulps(b, e))
+        else:
+            assert abs(b - e) <= 1e-310, (x, b, e)
+    assert worst <= 2, worst
+
+
+def test_table_expm1_exp_accuracy(tmp_path):
+    so = str(tmp_path / "fm3.so")
+    subprocess.run(["g++", "-O2", "-ffp-contract=off", "-shared", "-fPIC", "-o", so,
+                    os.path.join(ROOT, "tests", "native", "fastmath_host.cpp")], check=True)
+    L = ctypes.CDLL(so)
+    L.fm_expm1_exp_tab.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_long]
+    mpmath.mp.dps = 50
+    rng = np.random.default_rng(12)
+    xs = np.concatenate([rng.uniform(-745, 0, 2000), rng.uniform(-1, 1, 2000), rng.uniform(-0.02, 0.02, 2000),
+                         rng.uniform(-1e-5, 1e-5, 500), rng.uniform(0, 700, 500), -np.logspace(-300, 2.8, 300),
+                         np.logspace(-300, 2.8, 300), [0.0, 0.0027076, -0.0027076, 0.00135, -0.00135]])
+    em, q = np.empty_like(xs), np.empty_like(xs)
+    L.fm_expm1_exp_tab(xs.ctypes.data, em.ctypes.data, q.ctypes.data, xs.size)
+    wq = we = 0.0
+    for x, a, b in zip(xs, em, q):
+        eq = float(mpmath.exp(mpmath.mpf(x)))
+        eem = float(mpmath.expm1(mpmath.mpf(x)))
+        if eq >= 2.2250738585072014e-308:
+            wq = max(wq, _ulps(b, eq))
+        else:
+            assert abs(b - eq) <= 1e-310, (x, b, eq)
+        we = max(we, _ulps(a, eem))
+    assert wq <= 3 and we <= 4, (wq, we)
+
+
 def test_special_arguments(fm):
     em, q = fm([-np.inf, -800.0, 710.0, 0.0])
     assert q[0] == 0.0 and em[0] == -1.0 and q[1] == 0.0
