@@ -245,7 +245,7 @@ def run_ours(args):
     from paper_2307_03307_b200 import Solver, build as B
     ws, rk, lr = dist_env()
     torch.cuda.set_device(lr)
-    if ws > 1:
+    if ws > 1 or args.shard:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
     B.build()
@@ -257,7 +257,7 @@ def run_ours(args):
     gs = graph_stats(G)
     # c4 / c5 shard their edges over the ranks (one allreduce of d^(y) per iteration, DESIGN.md
     # §7); the small configs run one replica per GPU
-    sharded = ws > 1 and args.workload in ("c4", "c5")
+    sharded = (ws > 1 or args.shard) and args.workload in ("c4", "c5")
     make = Solver.graph_distributed if sharded else Solver.graph
     S = make(kind, G.src, G.dst, G.n_vertices, G.n_left if kind == "bmatch" else 0, max_iter=args.max_iter)
     st0 = S.stats()
@@ -415,12 +415,20 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--solve", action="store_true", help="also time a full solve (time to (1+eps) solution)")
+    ap.add_argument("--shard", action="store_true", help="sharded engine even with one rank (plumbing check)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
-    return run_ours(args)
+    rc = run_ours(args)
+    try:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()
+    except Exception:
+        pass
+    return rc
 
 
 if __name__ == "__main__":

@@ -86,6 +86,7 @@ struct mwu_ctx {
   int32_t* rowidC = nullptr; // fastC domset: row id of every nonzero of C = I + A
   // multi-GPU (edge-sharded): this rank owns internal edges [e0, e0 + E)
   int world = 1, rank = 0;
+  int sharded = 0;                            // a communicator drives the exchange (world >= 1)
   Comm* comm = nullptr;
   int64_t Eg = 0, ng = 0, mCg = 0, e0 = 0;   // global edges / variables / covering rows
   uint32_t* perm_full = nullptr;
@@ -303,13 +304,16 @@ void init_ctx_common(mwu_ctx* c, const mwu_options* opt) {
   if (opt) c->opt = *opt; else mwu_default_options(&c->opt);
   c->world = c->opt.world > 1 ? c->opt.world : 1;
   c->rank = c->world > 1 ? c->opt.rank : 0;
-  if (c->world > 1) {
+  // a communicator is built for world > 1, and also for world = 1 when an NCCL id or a rank
+  // group is passed (the sharded engine with one rank: exercises the exchange plumbing)
+  if (c->world > 1 || c->opt.nccl_id || c->opt.comm_group) {
     if (c->rank < 0 || c->rank >= c->world) throw MwuError{MWU_ERR_ARG, "rank out of range"};
     c->opt.use_graph = 0;                    // collectives are host-orchestrated
     try {
       if (c->opt.comm_group) c->comm = new SimComm((SimGroup*)c->opt.comm_group, c->rank);
       else if (c->opt.nccl_id) c->comm = new NcclComm(c->world, c->rank, c->opt.nccl_id);
       else throw std::runtime_error("world > 1 needs nccl_id or comm_group");
+      c->sharded = 1;
     } catch (const std::exception& e) { throw MwuError{MWU_ERR_NCCL, e.what()}; }
   }
   if (c->opt.device >= 0) CK(cudaSetDevice(c->opt.device));
@@ -484,7 +488,7 @@ void shard_range(int64_t n, int world, int rank, int64_t& a, int64_t& b) {
 
 // complete a deferred partial reduction: gather every rank's slots, combine in rank order
 void exchange(mwu_ctx* c) {
-  if (c->world <= 1) return;
+  if (!c->sharded) return;
   try {
     c->comm->allgather(c->ctl->dslots, c->gslots, MWU_SLOTS, c->st);
   } catch (const std::exception& e) { throw MwuError{MWU_ERR_NCCL, e.what()}; }
@@ -493,7 +497,7 @@ void exchange(mwu_ctx* c) {
 }
 
 void allreduce_rows(mwu_ctx* c, double* v, int64_t n) {
-  if (c->world <= 1) return;
+  if (!c->sharded) return;
   try {
     c->comm->allreduce_sum(v, n, c->st);
   } catch (const std::exception& e) { throw MwuError{MWU_ERR_NCCL, e.what()}; }
@@ -504,7 +508,7 @@ void localize(mwu_ctx* c) {
   const int w = (c->kind == K_DENSEST) ? 2 : 1;
   c->Eg = c->E; c->ng = c->n; c->mCg = c->mC;
   c->perm_full = c->perm;
-  if (c->world <= 1) return;
+  if (!c->sharded) return;
   int64_t a, b;
   shard_range(c->Eg, c->world, c->rank, a, b);
   c->e0 = a;
@@ -519,7 +523,7 @@ void localize(mwu_ctx* c) {
 
 // full internal-order vector of an edge-indexed quantity (w per edge) from every rank's slice
 const double* gather_full(mwu_ctx* c, const double* local, int w) {
-  if (c->world <= 1) return local;
+  if (!c->sharded) return local;
   int64_t maxE = 0;
   for (int r = 0; r < c->world; ++r) { int64_t a, b; shard_range(c->Eg, c->world, r, a, b); maxE = std::max(maxE, b - a); }
   if (!c->gfull) { c->gfull = dalloc<double>(c, w * c->Eg); c->gsend = dalloc<double>(c, w * maxE * c->world + w * maxE); }
@@ -797,7 +801,7 @@ void enqueue_search(mwu_ctx* c, cudaStream_t st) {
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>(2 * c->sms, chunks));   // 2 CTAs / SM
   SearchArgs A;
   int64_t p0 = 0, p1 = c->mP;                // sharded: each rank sums a slice of the replicated rows
-  if (c->world > 1) {
+  if (c->sharded) {
     shard_range(c->mP, c->world, c->rank, p0, p1);
     p0 &= ~int64_t(1);                       // 16-byte aligned bulk copies
     if (c->rank + 1 < c->world) p1 &= ~int64_t(1);
@@ -897,7 +901,7 @@ void probe_begin(mwu_ctx* c, double bound, double eps) {
   h.bisect_depth = c->opt.bisect_depth;
   h.use_graph = c->opt.use_graph;
   h.lazyC = c->lazyC;
-  h.world = c->world;
+  h.world = c->sharded ? std::max(2, c->world) : 1;   // device: defer partial reductions when sharded
   for (int i = 0; i < 32; ++i) h.aguess[i] = c->aguess[i];
   h.status = c->empty_cover ? ST_INFEASIBLE : ST_RUNNING;
   h.reason = c->empty_cover ? R_EMPTY_COVER : R_NONE;
@@ -939,7 +943,7 @@ void host_iteration(mwu_ctx* c, double alpha) {
   pull_ctl(c);
   if (c->hctl->status != ST_RUNNING) return;
   enqueue_column(c, c->st);
-  if (c->world > 1) {
+  if (c->sharded) {
     allreduce_rows(c, c->dy, c->mP);         // the one vector exchange per iteration
     exchange(c);                             // column reductions (max d, sums, inactive rows)
     if (c->lazyC) {
@@ -1022,7 +1026,7 @@ void profile_iters(mwu_ctx* c, int64_t k, double* out) {
     if (c->hctl->status != ST_RUNNING) break;
     timed(0, [&] {
       enqueue_column(c, c->st);
-      if (c->world > 1) {
+      if (c->sharded) {
         allreduce_rows(c, c->dy, c->mP);
         exchange(c);
         if (c->lazyC) {
@@ -1096,7 +1100,7 @@ void brackets(mwu_ctx* c, double eps, double& L, double& H) {
   // packing: witness x0 / max(P x0) (x0 of P:272), H = sum_i max_j 1/p_ji
   Ctl& h = *c->hctl;
   memset(&h, 0, sizeof(Ctl));
-  h.eps = eps; h.invB = 1.0; h.status = ST_RUNNING; h.iter_stop = INT64_MAX; h.world = c->world;
+  h.eps = eps; h.invB = 1.0; h.status = ST_RUNNING; h.iter_stop = INT64_MAX; h.world = c->sharded ? std::max(2, c->world) : 1;
   CK(cudaMemcpyAsync(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, c->st));
   init_x<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->x, c->kind == K_CSR ? c->colmaxP : nullptr, 1.0, c->ctl,
                                                   c->part, c->counter, c->ng > 0 ? c->ng : c->n);
@@ -1310,7 +1314,7 @@ mwu_status mwu_create_graph(const mwu_graph* g, const mwu_options* opt, mwu_ctx*
     }
     if (c->scatterP) build_blocked_order(c);
     fill_static_stats(c);                    // global sizes
-    if (c->world > 1 && !c->scatterP)
+    if (c->sharded && !c->scatterP)
       throw MwuError{MWU_ERR_ARG, "multi-GPU sharding needs an edge-variable kind (bmatch, match, densest) with deterministic = 0"};
     localize(c);
     alloc_vectors(c);

@@ -203,7 +203,7 @@ class Solver:
         rank 0 creates the NCCL id, every rank passes the same full edge list."""
         import torch.distributed as dist
         ws, rk = dist.get_world_size(), dist.get_rank()
-        uid = share_unique_id(get_unique_id)
+        uid = share_unique_id(get_unique_id)     # world 1 too: the exchange runs through NCCL
         return cls.graph(kind, src, dst, n_vertices, n_left, world=ws, rank=rk, nccl_id=uid, **opts)
 
     @classmethod

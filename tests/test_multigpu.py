@@ -156,3 +156,33 @@ def test_sharded_solve(cuda_ok, ci):
     assert any(abs(st0["objective"] - q) <= 1e-6 * abs(q) for q in refs), (st0["objective"], refs)
     lp = O.graph_lp(kind, s, d, G.n_vertices, st0["bound"])
     assert (lp.C @ x0).min() >= 1 - 1e-9                      # Theorem contract on the exact LP
+
+
+@pytest.mark.gpu
+def test_nccl_plumbing_one_rank(cuda_ok):
+    """The NCCL communicator (dlopen'ed library, unique id through torch.distributed, allreduce
+    and allgather on the library's stream) driving the sharded engine with one rank: the same
+    iterates as the plain engine.  (Several ranks need several GPUs; the sharding itself is
+    covered by the SimGroup tests above.)"""
+    from paper_2307_03307_b200 import Solver
+    port = _free_port()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        kind, G, eps = CASES[0]
+        s, d = G.numpy()
+        r = O.solve(kind, s, d, G.n_vertices, eps=eps, max_iter=300)
+        B = [p[0] for p in r.probes if p[1] == O.FEASIBLE][-1]
+        one = _solver(kind, G)
+        S = Solver.graph_distributed(kind, G.src.cuda(), G.dst.cuda(), G.n_vertices, 0)
+        for T in (one, S):
+            T.probe_begin(B, eps)
+            for _ in range(15):
+                T.step(1.0)
+        for k in ("x", "y", "z", "d", "dy"):
+            a, b = S.vec(k).cpu().numpy(), one.vec(k).cpu().numpy()
+            assert np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)) <= 1e-10, k
+        out = S.solve(eps, 300)
+        assert out == "feasible"
+    finally:
+        dist.destroy_process_group()
