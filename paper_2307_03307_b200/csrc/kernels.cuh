@@ -1241,19 +1241,29 @@ __device__ __forceinline__ bool act_bit(const uint32_t* act, int e) { return (__
 // shared memory by the bulk-copy engine (cp.async.bulk + mbarrier) kColStages tiles ahead; the
 // u gathers of tile i+1 are issued (registers) before tile i is computed.  Stages are released per warp (an 8-arrival "empty" mbarrier), so
 // only the producer thread waits for the slowest warp; no block-wide barrier in the loop.
-constexpr int kColStages = 4;
+#ifndef MWU_COL_DENSE_XD
+#define MWU_COL_DENSE_XD 0    // 1: stage x and d of every edge too (measured slower: 2 stages only)
+#endif
+constexpr int kColStages = MWU_COL_DENSE_XD ? 2 : 4;
 constexpr int kColOffS = MWU_CT * 8, kColOffD = kColOffS + MWU_CT * 4, kColOffA = kColOffD + MWU_CT * 4;
-constexpr int kColStageBytes = ((kColOffA + (MWU_CT / 32) * 4) + 127) / 128 * 128;
+constexpr int kColOffX = ((kColOffA + (MWU_CT / 32) * 4) + 127) / 128 * 128;   // x pairs, then d pairs
+constexpr int kColOffDD = kColOffX + MWU_CT * 16;
+constexpr int kColStageBytes = MWU_COL_DENSE_XD ? kColOffDD + MWU_CT * 16 : kColOffX;
 constexpr size_t kColSmem = (size_t)kColStages * kColStageBytes;
 
 __device__ __forceinline__ uint32_t r16(uint32_t b) { return (b + 15u) & ~15u; }
 
 __device__ __forceinline__ void col_issue(char* stage, uint64_t* bar, int tile, int E, const double* z,
-                                          const int32_t* srow, const int32_t* drow, const uint32_t* act) {
+                                          const int32_t* srow, const int32_t* drow, const uint32_t* act,
+                                          const double* x, const double* d) {
   const int e0 = tile * MWU_CT;
   const int rows = min(MWU_CT, E - e0);
   const uint32_t bz = r16(rows * 8u), bi = r16(rows * 4u), ba = r16(((rows + 31) / 32) * 4u);
-  mbar_expect_tx(bar, bz + 2 * bi + ba);
+  mbar_expect_tx(bar, bz + 2 * bi + ba + (MWU_COL_DENSE_XD ? 2 * rows * 16u : 0u));
+  if (MWU_COL_DENSE_XD) {
+    tma_load_1d(stage + kColOffX, x + 2 * (int64_t)e0, rows * 16u, bar);
+    tma_load_1d(stage + kColOffDD, d + 2 * (int64_t)e0, rows * 16u, bar);
+  }
   const uint64_t pf = pol_first();
   tma_load_1d_hint(stage, z + e0, bz, bar, pf);
   tma_load_1d_hint(stage + kColOffS, srow + e0, bi, bar, pf);
@@ -1302,7 +1312,7 @@ __global__ void __launch_bounds__(MWU_NT, 2) col_densest_fast(
   __syncthreads();
   if (threadIdx.x == 0)
     for (int k = 0; k < mine && k < kColStages; ++k)
-      col_issue(csm + k * kColStageBytes, &full[k], blockIdx.x + k * gridDim.x, E, z, srow, drow, act);
+      col_issue(csm + k * kColStageBytes, &full[k], blockIdx.x + k * gridDim.x, E, z, srow, drow, act, x, d);
   double us[kColEdges], ud[kColEdges], nus[kColEdges], nud[kColEdges];
   if (mine > 0) {
     mbar_wait(&full[0], 0u);
@@ -1335,7 +1345,12 @@ __global__ void __launch_bounds__(MWU_NT, 2) col_densest_fast(
       const int j = k * MWU_NT + threadIdx.x;
       pw[k] = j < rows ? sac[j >> 5] : 0u;
       had[k] = (pw[k] >> lane) & 1u;
-      if (had[k]) { xe[k] = x2[e0 + j]; dp[k] = d2[e0 + j]; }
+      if (MWU_COL_DENSE_XD) {
+        if (j < rows) {
+          xe[k] = reinterpret_cast<const double2*>(stg + kColOffX)[j];
+          dp[k] = reinterpret_cast<const double2*>(stg + kColOffDD)[j];
+        }
+      } else if (had[k]) { xe[k] = x2[e0 + j]; dp[k] = d2[e0 + j]; }
     }
     int nact = 0;
 #pragma unroll
@@ -1370,7 +1385,7 @@ __global__ void __launch_bounds__(MWU_NT, 2) col_densest_fast(
         if (gdbg) { gdbg[2 * e] = g0; gdbg[2 * e + 1] = g1; hdbg[2 * e] = h; hdbg[2 * e + 1] = h; }
         // g >= h gives fl(g/h) >= 1, i.e. d = 0 exactly
         const bool a0 = g0 < h, a1 = g1 < h;
-        if ((a0 || a1) && !had[k]) xe[k] = x2[e];                 // newly active: fetch x
+        if (!MWU_COL_DENSE_XD && (a0 || a1) && !had[k]) xe[k] = x2[e];   // newly active: fetch x
         if (a0) d0 = mwu_direction(g0, h, xe[k].x, sigma);
         if (a1) d1 = mwu_direction(g1, h, xe[k].y, sigma);
       }
@@ -1409,7 +1424,7 @@ __global__ void __launch_bounds__(MWU_NT, 2) col_densest_fast(
     if (lane == 31) tcnt[tile * (MWU_NT / 32) + warp] = incl;
     if (threadIdx.x == 0 && kt + kColStages < mine) {           // producer: refill once all warps left
       mbar_wait(&empty[slot], (uint32_t)((kt / kColStages) & 1));
-      col_issue(stg, &full[slot], blockIdx.x + (kt + kColStages) * gridDim.x, E, z, srow, drow, act);
+      col_issue(stg, &full[slot], blockIdx.x + (kt + kColStages) * gridDim.x, E, z, srow, drow, act, x, d);
     }
   };
   for (int kt = 0; kt < mine; ++kt) {
