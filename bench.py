@@ -255,9 +255,10 @@ def run_ours(args):
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t0
     gs = graph_stats(G)
-    # c4 / c5 shard their edges over the ranks (one allreduce of d^(y) per iteration, DESIGN.md
-    # §7); the small configs run one replica per GPU
-    sharded = (ws > 1 or args.shard) and args.workload in ("c4", "c5")
+    # c4 / c5 shard their edges (one allreduce of d^(y) per iteration), c2 / c3 their covering
+    # rows (one allreduce of the column gradient per iteration); c1 (10^4 edges)
+    # runs one replica per GPU
+    sharded = (ws > 1 or args.shard) and args.workload in ("c2", "c3", "c4", "c5")
     make = Solver.graph_distributed if sharded else Solver.graph
     S = make(kind, G.src, G.dst, G.n_vertices, G.n_left if kind == "bmatch" else 0, max_iter=args.max_iter)
     st0 = S.stats()
@@ -374,8 +375,10 @@ def run_ours(args):
                    "n_vars": stats["n"], "m_P": stats["m_P"], "m_C": stats["m_C"], "nnz": nnz_iter,
                    "edges": gs["E"], "first_bound": math.sqrt(L * H),
                    "l2": "inputs larger than L2 (per-vector GBs)",
-                   "parallelism": (f"edge-sharded x{ws} (NCCL allreduce of d^(y) per iteration)" if sharded
-                                   else (f"replicas x{ws}" if ws > 1 else "1 GPU"))},
+                   "parallelism": ((f"edge-sharded x{ws} (NCCL allreduce of d^(y) per iteration)"
+                                    if kind in ("densest", "bmatch") else
+                                    f"row-sharded x{ws} (NCCL allreduce of the column gradient per iteration)")
+                                   if sharded else (f"replicas x{ws}" if ws > 1 else "1 GPU"))},
         "nnz_per_s": nnz_iter * value,
         "iteration_roofline": {"bytes_alg_per_iter": balg, "achieved_gbs": balg / (ms_per_step / 1000) / 1e9,
                                "frac_of_8TBs": balg / (ms_per_step / 1000) / 8e12,

@@ -18,6 +18,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <chrono>
 #include <condition_variable>
 #include <mutex>
 #include <stdexcept>
@@ -115,11 +116,14 @@ struct SimGroup {
   std::vector<double*> out;
   std::vector<cudaStream_t> st;
   explicit SimGroup(int w) : world(w), in(w), out(w), st(w) {}
+  // a rank that failed (and will never arrive) turns the others' wait into an error after
+  // 120 s instead of a hang
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
     const int64_t g = gen;
     if (++arrived == world) { arrived = 0; ++gen; cv.notify_all(); }
-    else cv.wait(lk, [&] { return gen != g; });
+    else if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g; }))
+      throw std::runtime_error("SimGroup barrier timeout (another rank failed)");
   }
 };
 

@@ -403,12 +403,13 @@ __device__ void finalize(Ctl* c, int action, double* r) {
 // Phase reductions over rank-local rows are partial on a sharded run: the last block parks its
 // reduced slots in the control block and the host exchanges them (allgather) before
 // finalize_multi combines them in rank order and runs the same control logic on every rank.
-__device__ __forceinline__ bool partial_action(int a) {
-  return a == A_COL || a == A_COL_FAST || a == A_SEARCH || a == A_INIT_SING || a == A_INIT_EXT ||
-         a == A_INIT_W || a == A_VI_EXACT || a == A_SUM;
+__device__ __forceinline__ bool partial_action(const Ctl* c, int a) {
+  if (a == A_COL || a == A_INIT_SING || a == A_SUM) return !c->repvars;   // over the (local) variables
+  if (a == A_UPDATE) return c->partupd;                                  // local covering rows
+  return a == A_COL_FAST || a == A_SEARCH || a == A_INIT_EXT || a == A_INIT_W || a == A_VI_EXACT;
 }
 __device__ void finish(Ctl* c, int action, double* res, const int* ops, int n) {
-  if (c->world > 1 && partial_action(action)) {
+  if (c->world > 1 && partial_action(c, action)) {
     for (int s = 0; s < n; ++s) { c->dslots[s] = res[s]; c->dops[s] = ops[s]; }
     c->dn = n;
     c->daction = action;
@@ -426,7 +427,7 @@ __global__ void finalize_multi(Ctl* c, const double* __restrict__ g, int world) 
   for (int s = 0; s < MWU_SLOTS; ++s) res[s] = 0.0;
   for (int s = 0; s < n; ++s) {
     int op = c->dops[s];
-    if (act == A_INIT_W && s == 0) op = OP_FIRST;     // S_P of the replicated packing rows
+    if ((act == A_INIT_W || act == A_UPDATE) && s == 0) op = OP_FIRST;   // S_P of the replicated packing rows
     double a = g[s];
     for (int r = 1; r < world; ++r) {
       const double b = g[(size_t)r * MWU_SLOTS + s];
@@ -1538,7 +1539,7 @@ __global__ void __launch_bounds__(MWU_NT) vc_scatter(int64_t E, const int32_t* _
 // CSR rows sorted (row id per nonzero): out_r += w[col_k] (all values 1.0: C = I + A)
 __global__ void __launch_bounds__(MWU_NT) csr_scatter(int64_t nnz, const int32_t* __restrict__ rowid,
                                                       const uint32_t* __restrict__ col, const double* __restrict__ w,
-                                                      double* __restrict__ out, const Ctl* c) {
+                                                      double* __restrict__ out, const Ctl* c, int64_t row_base) {
   if (c->status != ST_RUNNING) return;
   constexpr int U = 4;
   const int64_t chunk = (int64_t)U * MWU_NT;
@@ -1556,9 +1557,18 @@ __global__ void __launch_bounds__(MWU_NT) csr_scatter(int64_t nnz, const int32_t
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       double run;
-      if (warp_run_sum(r[k], val[k], run) && r[k] >= 0) red_add_f64(out + r[k], run);
+      if (warp_run_sum(r[k], val[k], run) && r[k] >= 0) red_add_f64(out + (r[k] - row_base), run);
     }
   }
+}
+
+// Sharded domset: the local rows' contribution to C^T v (C symmetric): out[col_k] += w[row_k - base]
+__global__ void __launch_bounds__(MWU_NT) csr_scatter_T(int64_t nnz, const int32_t* __restrict__ rowid,
+                                                        const uint32_t* __restrict__ col, const double* __restrict__ w,
+                                                        int64_t row_base, double* __restrict__ out, const Ctl* c) {
+  if (c->status != ST_RUNNING) return;
+  for (int64_t q = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; q < nnz; q += (int64_t)gridDim.x * MWU_NT)
+    red_add_f64(out + __ldcs(col + q), __ldg(w + (__ldcs(rowid + q) - row_base)));
 }
 
 // Column epilogue over the variables (pure covering, P = (1/M) 1^T): lazy x += alpha d,

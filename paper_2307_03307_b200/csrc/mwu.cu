@@ -89,6 +89,8 @@ struct mwu_ctx {
   int sharded = 0;                            // a communicator drives the exchange (world >= 1)
   Comm* comm = nullptr;
   int64_t Eg = 0, ng = 0, mCg = 0, e0 = 0;   // global edges / variables / covering rows
+  std::vector<int64_t> rb;                    // [world+1] ranges of the sharded dimension
+  int64_t r0 = 0, k0 = 0, nnzL = 0;           // domset: first local row, first local nonzero, count
   uint32_t* perm_full = nullptr;
   double* gslots = nullptr;                   // [world][MWU_SLOTS] gathered reduction slots
   double* gfull = nullptr;                    // full internal-order vector (hooks)
@@ -509,32 +511,62 @@ void localize(mwu_ctx* c) {
   c->Eg = c->E; c->ng = c->n; c->mCg = c->mC;
   c->perm_full = c->perm;
   if (!c->sharded) return;
-  int64_t a, b;
-  shard_range(c->Eg, c->world, c->rank, a, b);
+  c->gslots = dalloc<double>(c, (int64_t)c->world * MWU_SLOTS);
+  c->rb.assign(c->world + 1, 0);
+  if (c->kind == K_DOMSET) {
+    // covering rows (vertices) by nnz-balanced ranges on even rows (16-byte aligned row slices)
+    std::vector<int64_t> rp(c->nv + 1);
+    CK(cudaMemcpy(rp.data(), c->csrC.rowptr, (c->nv + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    for (int r = 1; r < c->world; ++r) {
+      const int64_t target = (int64_t)((__int128)c->nnzC * r / c->world);
+      int64_t row = std::lower_bound(rp.begin(), rp.end(), target) - rp.begin();
+      row &= ~int64_t(1);
+      c->rb[r] = std::max(c->rb[r - 1], std::min(row, c->nv));
+    }
+    c->rb[c->world] = c->nv;
+    c->r0 = c->rb[c->rank];
+    c->mC = c->rb[c->rank + 1] - c->r0;
+    c->k0 = rp[c->r0];
+    c->nnzL = rp[c->r0 + c->mC] - c->k0;
+    return;                                    // variables (vertices) replicated
+  }
+  for (int r = 0; r <= c->world; ++r) {
+    int64_t a, b;
+    shard_range(c->Eg, c->world, std::min(r, c->world - 1), a, b);
+    c->rb[r] = (r == c->world) ? c->Eg : a;
+  }
+  const int64_t a = c->rb[c->rank], b = c->rb[c->rank + 1];
   c->e0 = a;
   c->E = b - a;
+  if (c->kind == K_VCOVER) {                   // covering rows = edges local, vertices replicated
+    c->mC = c->E;
+    c->src += a;
+    c->dst += a;
+    return;
+  }
   c->n = w * c->E;
   if (c->kind == K_DENSEST) c->mC = c->E;
   c->srow += a;
   c->drow += a;
   c->perm += a;
-  c->gslots = dalloc<double>(c, (int64_t)c->world * MWU_SLOTS);
 }
 
-// full internal-order vector of an edge-indexed quantity (w per edge) from every rank's slice
+// full vector of a sharded quantity (w per item of the sharded dimension: edges, or domset
+// rows) from every rank's slice
 const double* gather_full(mwu_ctx* c, const double* local, int w) {
   if (!c->sharded) return local;
+  const int64_t total = c->rb[c->world];
   int64_t maxE = 0;
-  for (int r = 0; r < c->world; ++r) { int64_t a, b; shard_range(c->Eg, c->world, r, a, b); maxE = std::max(maxE, b - a); }
-  if (!c->gfull) { c->gfull = dalloc<double>(c, w * c->Eg); c->gsend = dalloc<double>(c, w * maxE * c->world + w * maxE); }
+  for (int r = 0; r < c->world; ++r) maxE = std::max(maxE, c->rb[r + 1] - c->rb[r]);
+  if (!c->gfull) { c->gfull = dalloc<double>(c, w * total); c->gsend = dalloc<double>(c, w * maxE * c->world + w * maxE); }
   double* recv = c->gsend + w * maxE;
-  CK(cudaMemcpyAsync(c->gsend, local, w * c->E * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+  const int64_t mine = c->rb[c->rank + 1] - c->rb[c->rank];
+  if (mine > 0) CK(cudaMemcpyAsync(c->gsend, local, w * mine * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
   try {
     c->comm->allgather(c->gsend, recv, w * maxE, c->st);
   } catch (const std::exception& e) { throw MwuError{MWU_ERR_NCCL, e.what()}; }
   for (int r = 0; r < c->world; ++r) {
-    int64_t a, b;
-    shard_range(c->Eg, c->world, r, a, b);
+    const int64_t a = c->rb[r], b = c->rb[r + 1];
     if (b > a) CK(cudaMemcpyAsync(c->gfull + w * a, recv + (int64_t)r * w * maxE, w * (b - a) * sizeof(double),
                                   cudaMemcpyDeviceToDevice, c->st));
   }
@@ -701,9 +733,13 @@ void enqueue_column(mwu_ctx* c, cudaStream_t st) {
         if (c->kind == K_VCOVER)
           vc_scatter<<<(int)std::min<int64_t>(4 * c->sms, (c->E + 4 * MWU_NT - 1) / (4 * MWU_NT) + 1), MWU_NT, 0, st>>>(
               c->E, c->src, c->dst, c->v, c->hsum, c->ctl);
-        else
+        else if (!c->sharded)
           csr_scatter<<<(int)std::min<int64_t>(4 * c->sms, (c->nnzC + 4 * MWU_NT - 1) / (4 * MWU_NT) + 1), MWU_NT, 0, st>>>(
-              c->nnzC, c->rowidC, c->csrC.idx, c->v, c->hsum, c->ctl);
+              c->nnzC, c->rowidC, c->csrC.idx, c->v, c->hsum, c->ctl, 0);
+        else   // local rows: C^T v by scattering each local row's weight to its columns (C symmetric)
+          csr_scatter_T<<<(int)std::min<int64_t>(4 * c->sms, (c->nnzL + 4 * MWU_NT - 1) / (4 * MWU_NT) + 1), MWU_NT, 0, st>>>(
+              c->nnzL, c->rowidC + c->k0, c->csrC.idx + c->k0, c->v, c->r0, c->hsum, c->ctl);
+        allreduce_rows(c, c->hsum, c->n);     // sharded: partial column gradient of the local rows
         col_vertex<<<rows_grid(c, c->n), MWU_NT, 0, st>>>(c->n, c->hsum, c->x, c->d, c->record ? c->gdbg : nullptr,
                                                         c->record ? c->hdbg : nullptr, c->ctl, c->part, c->counter);
         c->launches += 2;
@@ -774,9 +810,10 @@ void enqueue_forward(mwu_ctx* c, cudaStream_t st, const double* in, double* oy, 
       break;
     case K_DOMSET:
       if (c->fastC) {
-        CK(cudaMemsetAsync(oz, 0, c->mC * sizeof(double), st));
-        csr_scatter<<<(int)std::min<int64_t>(4 * c->sms, (c->nnzC + 4 * MWU_NT - 1) / (4 * MWU_NT) + 1), MWU_NT, 0, st>>>(
-            c->nnzC, c->rowidC, c->csrC.idx, in, oz, c->ctl);
+        CK(cudaMemsetAsync(oz, 0, (c->mC > 0 ? c->mC : 1) * sizeof(double), st));
+        const int64_t nz = c->sharded ? c->nnzL : c->nnzC;
+        csr_scatter<<<(int)std::min<int64_t>(4 * c->sms, (nz + 4 * MWU_NT - 1) / (4 * MWU_NT) + 1), MWU_NT, 0, st>>>(
+            nz, c->rowidC + c->k0, c->csrC.idx + c->k0, in, oz, c->ctl, c->r0);
         c->launches++;
         if (!init) { step_done<<<1, 32, 0, st>>>(c->ctl); c->launches++; }
         break;
@@ -902,6 +939,8 @@ void probe_begin(mwu_ctx* c, double bound, double eps) {
   h.use_graph = c->opt.use_graph;
   h.lazyC = c->lazyC;
   h.world = c->sharded ? std::max(2, c->world) : 1;   // device: defer partial reductions when sharded
+  h.repvars = c->fastC ? 1 : 0;                          // covering kinds: variables replicated
+  h.partupd = (c->sharded && c->fastC) ? 1 : 0;          // their covering rows are local
   for (int i = 0; i < 32; ++i) h.aguess[i] = c->aguess[i];
   h.status = c->empty_cover ? ST_INFEASIBLE : ST_RUNNING;
   h.reason = c->empty_cover ? R_EMPTY_COVER : R_NONE;
@@ -924,7 +963,7 @@ void probe_begin(mwu_ctx* c, double bound, double eps) {
   exchange(c);
   // y = P x, z = C x
   enqueue_forward(c, c->st, c->x, c->y, c->z, true);
-  allreduce_rows(c, c->y, c->mP);            // sharded: partial packing rows of the local edges
+  if (c->scatterP) allreduce_rows(c, c->y, c->mP);   // sharded: partial packing rows of the local edges
   init_ext<<<rows_grid(c, c->mP + c->mC), MWU_NT, 0, c->st>>>(c->mP, c->y, c->mC, c->z, c->ctl, c->part, c->counter);
   c->launches++;
   exchange(c);
@@ -943,7 +982,7 @@ void host_iteration(mwu_ctx* c, double alpha) {
   pull_ctl(c);
   if (c->hctl->status != ST_RUNNING) return;
   enqueue_column(c, c->st);
-  if (c->sharded) {
+  if (c->sharded && c->scatterP) {
     allreduce_rows(c, c->dy, c->mP);         // the one vector exchange per iteration
     exchange(c);                             // column reductions (max d, sums, inactive rows)
     if (c->lazyC) {
@@ -961,6 +1000,7 @@ void host_iteration(mwu_ctx* c, double alpha) {
     CKL();
   }
   enqueue_update(c, c->st, 1);
+  exchange(c);                               // sharded covering kinds: S_C over local rows
   CKL();
   sync(c);
   if (alpha > 0.0) push_field(c, &c->ctl->fixed_alpha, 0.0);
@@ -1026,7 +1066,7 @@ void profile_iters(mwu_ctx* c, int64_t k, double* out) {
     if (c->hctl->status != ST_RUNNING) break;
     timed(0, [&] {
       enqueue_column(c, c->st);
-      if (c->sharded) {
+      if (c->sharded && c->scatterP) {
         allreduce_rows(c, c->dy, c->mP);
         exchange(c);
         if (c->lazyC) {
@@ -1042,7 +1082,7 @@ void profile_iters(mwu_ctx* c, int64_t k, double* out) {
       timed(2, [&] { enqueue_search(c, c->st); exchange(c); });
       out[9] += 1;
     }
-    timed(3, [&] { enqueue_update(c, c->st, 1); });
+    timed(3, [&] { enqueue_update(c, c->st, 1); exchange(c); });
     out[8] += 1;
   }
   cudaEventDestroy(e[0]);
@@ -1081,7 +1121,8 @@ void brackets(mwu_ctx* c, double eps, double& L, double& H) {
     return;
   }
   if (c->kind == K_VCOVER || c->kind == K_DOMSET) {
-    L = (c->kind == K_VCOVER) ? (double)c->E / (double)c->maxdeg : (double)c->nv / (double)(c->maxdeg + 1);
+    L = (c->kind == K_VCOVER) ? (double)(c->Eg > 0 ? c->Eg : c->E) / (double)c->maxdeg
+                              : (double)c->nv / (double)(c->maxdeg + 1);
     if (c->kind == K_VCOVER) k_fill_nonzero<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->deg, c->xbest, 1.0);
     else k_fill<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->xbest, 1.0);
     CKL();
@@ -1101,13 +1142,14 @@ void brackets(mwu_ctx* c, double eps, double& L, double& H) {
   Ctl& h = *c->hctl;
   memset(&h, 0, sizeof(Ctl));
   h.eps = eps; h.invB = 1.0; h.status = ST_RUNNING; h.iter_stop = INT64_MAX; h.world = c->sharded ? std::max(2, c->world) : 1;
+  h.repvars = c->fastC ? 1 : 0;
   CK(cudaMemcpyAsync(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, c->st));
   init_x<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->x, c->kind == K_CSR ? c->colmaxP : nullptr, 1.0, c->ctl,
                                                   c->part, c->counter, c->ng > 0 ? c->ng : c->n);
   CKL();
   exchange(c);
   enqueue_forward(c, c->st, c->x, c->y, c->z, true);
-  allreduce_rows(c, c->y, c->mP);
+  if (c->scatterP) allreduce_rows(c, c->y, c->mP);
   reduce_dev(c, c->y, c->mP, s, mx);
   CK(cudaMemcpyAsync(c->tmp, &mx, sizeof(double), cudaMemcpyHostToDevice, c->st));
   scale_div<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->x, c->xbest, c->tmp);
@@ -1314,10 +1356,19 @@ mwu_status mwu_create_graph(const mwu_graph* g, const mwu_options* opt, mwu_ctx*
     }
     if (c->scatterP) build_blocked_order(c);
     fill_static_stats(c);                    // global sizes
-    if (c->sharded && !c->scatterP)
-      throw MwuError{MWU_ERR_ARG, "multi-GPU sharding needs an edge-variable kind (bmatch, match, densest) with deterministic = 0"};
+    if (c->sharded && !c->scatterP && !c->fastC)
+      throw MwuError{MWU_ERR_ARG, "multi-GPU sharding needs a graph kind with deterministic = 0"};
     localize(c);
     alloc_vectors(c);
+    {                                        // exchange flags for reductions before a probe
+      Ctl& h = *c->hctl;
+      memset(&h, 0, sizeof(Ctl));
+      h.world = c->sharded ? std::max(2, c->world) : 1;
+      h.repvars = c->fastC ? 1 : 0;
+      h.partupd = (c->sharded && c->fastC) ? 1 : 0;
+      CK(cudaMemcpyAsync(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, c->st));
+      sync(c);
+    }
     CK(cudaEventRecord(b, c->st));
     CK(cudaEventSynchronize(b));
     float ms = 0; CK(cudaEventElapsedTime(&ms, a, b));
@@ -1548,6 +1599,8 @@ mwu_status mwu_get_vec(mwu_ctx* c, int which, double* out, int64_t len) {
         else { scale_div<<<rows_grid(c, c->mC), MWU_NT, 0, c->st>>>(c->mC, c->v, c->tmp, &c->ctl->SC); CKL(); src = c->tmp; }
         break;
     }
+    if (!c->perm && c->sharded && !use_scal && (which == MWU_VEC_Z || which == MWU_VEC_DZ || which == MWU_VEC_WC))
+      src = gather_full(c, src, 1);          // covering rows of every rank (vcover / domset)
     if (c->perm && !use_scal) {              // internal (L2-blocked) edge order -> original (Q29)
       const int w = (c->kind == K_DENSEST) ? 2 : 1;
       if (which == MWU_VEC_X || which == MWU_VEC_D || which == MWU_VEC_XBEST || which == MWU_VEC_G ||

@@ -82,7 +82,9 @@ def _run_ranks(world, fn):
     for t in th:
         t.start()
     for t in th:
-        t.join()
+        t.join(timeout=300)
+    if any(t.is_alive() for t in th):
+        raise RuntimeError("a rank did not finish")
     if errs:
         raise errs[0][1]
     return out
@@ -94,7 +96,8 @@ def _solver(kind, G, **kw):
 
 
 CASES = [("densest", gg.rmat(10, 16, seed=7), 0.1), ("bmatch", gg.bipartite_zipf(1024, 1024, 16384, seed=2), 0.1),
-         ("match", gg.hub_graph(6000, 2, 4000, 20000, seed=1), 0.1)]
+         ("match", gg.hub_graph(6000, 2, 4000, 20000, seed=1), 0.1),
+         ("vcover", gg.erdos_renyi(5000, 40000, seed=5), 0.05), ("domset", gg.rmat(12, 16, seed=6), 0.05)]
 
 
 @pytest.mark.gpu
@@ -110,7 +113,8 @@ def test_sharded_fixed_steps_match_single_gpu(cuda_ok, world, ci):
     one.probe_begin(B, eps)
     for _ in range(20):
         one.step(1.0)
-    ref = {k: one.vec(k).cpu().numpy() for k in ("x", "y", "d", "dy")}
+    keys = ("x", "y", "z", "d", "dy", "dz", "wc")
+    ref = {k: one.vec(k).cpu().numpy() for k in keys}
     grp = SimGroup(world)
 
     def rank_fn(rk):
@@ -118,7 +122,7 @@ def test_sharded_fixed_steps_match_single_gpu(cuda_ok, world, ci):
         S.probe_begin(B, eps)
         for _ in range(20):
             S.step(1.0)
-        return {k: S.vec(k).cpu().numpy() for k in ("x", "y", "d", "dy")}
+        return {k: S.vec(k).cpu().numpy() for k in keys}
     outs = _run_ranks(world, rank_fn)
     grp.close()
     for o in outs:
@@ -151,9 +155,17 @@ def test_sharded_solve(cuda_ok, ci):
     assert o0 == o1 == "feasible"
     assert np.array_equal(x0, x1)
     assert st0["bound"] == stb["bound"] and st0["probes"] == stb["probes"]
-    refs = [st1["objective"]] + [O.solve(kind, s, d, G.n_vertices, eps=eps, max_iter=400, x0_scale=sc).objective
-                                 for sc in (1.0, 1 + 2.0 ** -52, 1 - 2.0 ** -52)]
-    assert any(abs(st0["objective"] - q) <= 1e-6 * abs(q) for q in refs), (st0["objective"], refs)
+    runs = [O.solve(kind, s, d, G.n_vertices, eps=eps, max_iter=400, x0_scale=sc)
+            for sc in (1.0, 1 + 2.0 ** -52, 1 - 2.0 ** -52)]
+    if kind in ("vcover", "domset"):
+        # pure covering: the bisection's bound is the reproducible result; <1, x_out> depends
+        # on the (chaotic) final iterate even for the oracle's own one-ulp reruns
+        refs = [st1["bound"]] + [q.bound for q in runs]
+        assert any(abs(st0["bound"] - q) <= 1e-6 * abs(q) for q in refs), (st0["bound"], refs)
+        assert abs(st0["objective"] - st1["objective"]) <= eps * st1["objective"]
+    else:
+        refs = [st1["objective"]] + [q.objective for q in runs]
+        assert any(abs(st0["objective"] - q) <= 1e-6 * abs(q) for q in refs), (st0["objective"], refs)
     lp = O.graph_lp(kind, s, d, G.n_vertices, st0["bound"])
     assert (lp.C @ x0).min() >= 1 - 1e-9                      # Theorem contract on the exact LP
 
