@@ -576,10 +576,13 @@ const double* gather_full(mwu_ctx* c, const double* local, int w) {
 // Fast edge-variable kinds: L2-blocked internal edge order (storage.cuh k_block_keys) and the
 // endpoint rows of the internal order.  perm maps internal -> original edge ids (Q29 order is
 // restored by every vector hook and mwu_get_x).
-constexpr int kBlockL = 22, kBlockR = 20;   // src blocks of 4M vertices, dst blocks of 1M
+constexpr int kBlockLDefault = 22, kBlockRDefault = 20;   // src blocks of 4M vertices, dst blocks of 1M
 void build_blocked_order(mwu_ctx* c) {
   const int64_t E = c->E;
   if (E <= 0) return;
+  const char* eL = getenv("MWU_BLOCK_L");      // experiment knobs
+  const char* eR = getenv("MWU_BLOCK_R");
+  const int kBlockL = eL ? atoi(eL) : kBlockLDefault, kBlockR = eR ? atoi(eR) : kBlockRDefault;
   const int nbL = (int)((c->nv + (int64_t(1) << kBlockL) - 1) >> kBlockL);
   const int nbR = (int)((c->nv + (int64_t(1) << kBlockR) - 1) >> kBlockR);
   unsigned long long *keys = talloc<unsigned long long>(E), *kout = talloc<unsigned long long>(E);
