@@ -79,6 +79,7 @@ struct mwu_ctx {
   int lazyC = 0;
   int scatterP = 0;          // graph kinds with edge variables: d^(y) scattered by the column kernel
   uint32_t* perm = nullptr;  // scatterP: internal (L2-blocked) edge position -> original edge id
+  uint32_t* rowperm = nullptr;  // scatterP: fast (degree-ordered) packing row -> vertex-order row
   int fastC = 0;             // vcover / domset: transposed (and domset forward) products scattered
   double* exptab = nullptr;  // 2^(j/256), j < 256 (fastmath.cuh mwu_exp_tab)
   double* emtab = nullptr;   // 2^(j/256), j in [-128, 128), and 2^(j/256) - 1 as hi + lo
@@ -292,7 +293,7 @@ void alloc_vectors(mwu_ctx* c) {
   if (c->mP > mx) mx = c->mP;
   if (c->mC > mx) mx = c->mC;
   c->tmp = dalloc<double>(c, mx);
-  if (c->scatterP) c->tmp2 = dalloc<double>(c, c->ng > 0 ? c->ng : c->n);
+  if (c->scatterP) c->tmp2 = dalloc<double>(c, std::max(c->ng > 0 ? c->ng : c->n, c->mP));
   if (c->fastC) c->hsum = dalloc<double>(c, c->n);
   if (c->kind == K_CSR && !c->pSing && !c->cSing) c->gtmp = dalloc<double>(c, c->n);
   CK(cudaMemsetAsync(c->d, 0, c->n * sizeof(double), c->st));
@@ -596,7 +597,27 @@ void build_blocked_order(mwu_ctx* c) {
   CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, kout, vals, c->perm, E, 0, bits, c->st));
   void* t = talloc<char>(tb);
   CK(cub::DeviceRadixSort::SortPairs(t, tb, keys, kout, vals, c->perm, E, 0, bits, c->st));
-  k_map_endpoints_perm<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->perm, c->src, c->dst, c->prow, c->srow, c->drow);
+  // packing rows in degree-descending order (fast path only; hooks restore vertex order)
+  int32_t* prowf = talloc<int32_t>(c->nv);
+  {
+    unsigned long long *dk = talloc<unsigned long long>(c->nv), *dko = talloc<unsigned long long>(c->nv);
+    uint32_t *dv = talloc<uint32_t>(c->nv), *dvo = talloc<uint32_t>(c->nv);
+    k_deg_keys<<<grid_for(c, c->nv), MWU_NT, 0, c->st>>>(c->nv, c->deg, dk, dv);
+    CKL();
+    size_t tb2 = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, dk, dko, dv, dvo, c->nv, 0, 64, c->st));
+    void* t2 = talloc<char>(tb2);
+    CK(cub::DeviceRadixSort::SortPairs(t2, tb2, dk, dko, dv, dvo, c->nv, 0, 64, c->st));
+    c->rowperm = dalloc<uint32_t>(c, c->nprime);
+    k_deg_rows<<<grid_for(c, c->nprime), MWU_NT, 0, c->st>>>(c->nprime, dvo, c->prow, prowf, c->rowperm);
+    CKL();
+    sync(c);
+    tfree(t2); tfree(dk); tfree(dko); tfree(dv); tfree(dvo);
+  }
+  k_map_endpoints_perm<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->perm, c->src, c->dst, prowf, c->srow, c->drow);
+  CKL();
+  sync(c);
+  tfree(prowf);
   CKL();
   sync(c);
   tfree(t); tfree(keys); tfree(kout); tfree(vals);
@@ -1601,6 +1622,11 @@ mwu_status mwu_get_vec(mwu_ctx* c, int which, double* out, int64_t len) {
         }
         else { scale_div<<<rows_grid(c, c->mC), MWU_NT, 0, c->st>>>(c->mC, c->v, c->tmp, &c->ctl->SC); CKL(); src = c->tmp; }
         break;
+    }
+    if (c->rowperm && !use_scal && (which == MWU_VEC_Y || which == MWU_VEC_DY || which == MWU_VEC_WP)) {
+      k_unperm<<<grid_for(c, c->mP), MWU_NT, 0, c->st>>>(c->mP, c->rowperm, src, c->tmp2, 1);   // vertex order
+      CKL();
+      src = c->tmp2;
     }
     if (!c->perm && c->sharded && !use_scal && (which == MWU_VEC_Z || which == MWU_VEC_DZ || which == MWU_VEC_WC))
       src = gather_full(c, src, 1);          // covering rows of every rank (vcover / domset)

@@ -118,6 +118,24 @@ __global__ void k_block_keys(int64_t E, const int32_t* src, const int32_t* dst, 
   }
 }
 
+// degree-descending row order (hot rows of power-law graphs cluster in a small, L2-resident
+// prefix of the packing-row vectors): key = (~deg, v)
+__global__ void k_deg_keys(int64_t nv, const int32_t* deg, unsigned long long* keys, uint32_t* vals) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    keys[v] = ((unsigned long long)(0xffffffffu - (uint32_t)deg[v]) << 32) | (unsigned long long)v;
+    vals[v] = (uint32_t)v;
+  }
+}
+// sorted vertices -> fast row ids: prowf[v_i] = i (i < n'), rowperm[i] = prow[v_i]
+__global__ void k_deg_rows(int64_t nprime, const uint32_t* vsorted, const int32_t* prow, int32_t* prowf,
+                           uint32_t* rowperm) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nprime; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = vsorted[i];
+    prowf[v] = (int32_t)i;
+    rowperm[i] = (uint32_t)prow[v];
+  }
+}
+
 __global__ void k_map_endpoints_perm(int64_t E, const uint32_t* perm, const int32_t* src, const int32_t* dst,
                                      const int32_t* prow, int32_t* srow, int32_t* drow) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x) {
