@@ -1442,15 +1442,28 @@ __global__ void __launch_bounds__(MWU_NT, 2) col_densest_fast(
 // g_e = w_p[r(src)] + w_p[r(dst)] (M^T), d_e, and the forward product
 // d^(y) = M d scattered into the vertex vector (src side: warp-segmented runs of the sorted edge
 // list; dst side: one fp64 reduction per nonzero d_e).  Reduces max d and sum(d)/M.
+// Propagation blocking of the random (dst) side of the scattered forward product when the
+// packing-row vector is far beyond L2 (c5): the column kernel appends (row, value) to the bucket
+// of the row's 1M-row range (warp-aggregated cursor atomics, L2-combined writes), then
+// bucket_flush adds each bucket into its L2-resident 8 MB slice of d^(y), bucket after bucket.
+struct Buckets {
+  int32_t* row;          // [capacity] (nullptr: scatter directly)
+  double* val;
+  const int64_t* base;   // [nb + 1] static capacities (dst-row histogram of the local edges)
+  int32_t* cnt;          // [nb] fill of this iteration
+  int shift, nb;
+};
+
 __global__ void __launch_bounds__(MWU_NT, 3) col_match_fast(int64_t E, const int32_t* __restrict__ srow,
                                                          const int32_t* __restrict__ drow,
                                                          const double* __restrict__ u, double* __restrict__ x,
                                                          double* __restrict__ d, double* __restrict__ dy,
                                                          double* gdbg, double* hdbg, Ctl* c, double* part,
-                                                         unsigned int* counter) {
+                                                         unsigned int* counter, Buckets bk) {
   if (c->status != ST_RUNNING) return;
   const double rSP = 1.0 / c->SP, invB = c->invB, sigma = c->sigma, ap = c->alpha_prev;
   const int apply = c->apply_prev;
+  const int lane = threadIdx.x & 31;
   double acc[2] = {-INFINITY, 0.0};
   constexpr int U = 2;
   const int64_t chunk = (int64_t)U * MWU_NT;
@@ -1464,8 +1477,13 @@ __global__ void __launch_bounds__(MWU_NT, 3) col_match_fast(int64_t E, const int
       else { sr[k] = -1; dr[k] = -1; }
     }
 #pragma unroll
-    for (int k = 0; k < U; ++k)
+    for (int k = 0; k < U; ++k) {
+#if MWU_ABLATE == 1
+      if (sr[k] >= 0) { us[k] = __ldg(u + sr[k]); ud[k] = us[k]; }
+#else
       if (sr[k] >= 0) { us[k] = __ldg(u + sr[k]); ud[k] = __ldg(u + dr[k]); }
+#endif
+    }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const int64_t e = base + k * MWU_NT + threadIdx.x;
@@ -1478,9 +1496,32 @@ __global__ void __launch_bounds__(MWU_NT, 3) col_match_fast(int64_t E, const int
         if (gdbg) { gdbg[e] = g; hdbg[e] = invB; }
         acc[0] = fmax(acc[0], de);
         acc[1] += invB * de;
-        if (de > 0.0) red_add_f64(dy + dr[k], de);                // dst side
       }
-      if (__any_sync(0xffffffffu, de > 0.0)) {                    // src side: sorted runs
+      const bool want = de > 0.0;
+      if (bk.row) {                                               // dst side, bucketed
+        // warp-aggregated cursor per distinct bucket (full-mask intrinsics in a uniform loop)
+        const int b = want ? (dr[k] >> bk.shift) : -1;
+        unsigned m = __ballot_sync(0xffffffffu, want);
+        while (m) {
+          const int leader = __ffs(m) - 1;
+          const int lb = __shfl_sync(0xffffffffu, b, leader);
+          const unsigned grp = __ballot_sync(0xffffffffu, want && b == lb);
+          int pos = 0;
+          if (lane == leader) pos = atomicAdd(bk.cnt + lb, __popc(grp));
+          pos = __shfl_sync(0xffffffffu, pos, leader);
+          if (want && b == lb) {
+            const int64_t slot = bk.base[lb] + pos + __popc(grp & ((1u << lane) - 1u));
+            bk.row[slot] = dr[k];
+            bk.val[slot] = de;
+          }
+          m &= ~grp;
+        }
+      } else {
+#if MWU_ABLATE != 3
+        if (want) red_add_f64(dy + dr[k], de);                    // dst side
+#endif
+      }
+      if (__any_sync(0xffffffffu, want)) {                        // src side: sorted runs
         double run;
         if (warp_run_sum(sr[k], de, run) && run > 0.0) red_add_f64(dy + sr[k], run);
       }
@@ -1488,6 +1529,25 @@ __global__ void __launch_bounds__(MWU_NT, 3) col_match_fast(int64_t E, const int
   }
   const int ops[2] = {OP_MAX, OP_SUM};
   reduce_and_finalize<2>(acc, ops, part, counter, c, A_COL);
+}
+
+// Second half of the propagation blocking: slots in bucket order (the grid's window stays in one
+// or two buckets, whose d^(y) slice is L2-resident); unfilled capacity is skipped.
+__global__ void __launch_bounds__(MWU_NT) bucket_flush(int64_t cap, const int32_t* __restrict__ brow,
+                                                       const double* __restrict__ bval, const int64_t* __restrict__ base,
+                                                       const int32_t* __restrict__ cnt, int nb, double* __restrict__ dy,
+                                                       const Ctl* c) {
+  if (c->status != ST_RUNNING) return;
+  extern __shared__ int64_t sb[];               // [nb + 1] bases, then [nb] fills
+  int64_t* sfill = sb + nb + 1;
+  for (int i = threadIdx.x; i <= nb; i += MWU_NT) sb[i] = base[i];
+  for (int i = threadIdx.x; i < nb; i += MWU_NT) sfill[i] = cnt[i];
+  __syncthreads();
+  for (int64_t s = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; s < cap; s += (int64_t)gridDim.x * MWU_NT) {
+    int lo = 0, hi = nb - 1;                    // bucket of slot s: last b with base[b] <= s
+    while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (sb[mid] <= s) lo = mid; else hi = mid - 1; }
+    if (s - sb[lo] < sfill[lo]) red_add_f64(dy + __ldcs(brow + s), __ldcs(bval + s));
+  }
 }
 
 // Init forward product y = P x of the edge-variable kinds by scatter (fast path):

@@ -80,6 +80,8 @@ struct mwu_ctx {
   int scatterP = 0;          // graph kinds with edge variables: d^(y) scattered by the column kernel
   uint32_t* perm = nullptr;  // scatterP: internal (L2-blocked) edge position -> original edge id
   uint32_t* rowperm = nullptr;  // scatterP: fast (degree-ordered) packing row -> vertex-order row
+  Buckets bk{};                 // bmatch with an out-of-L2 packing side: propagation blocking
+  int64_t bkcap = 0;
   int fastC = 0;             // vcover / domset: transposed (and domset forward) products scattered
   double* exptab = nullptr;  // 2^(j/256), j < 256 (fastmath.cuh mwu_exp_tab)
   double* emtab = nullptr;   // 2^(j/256), j in [-128, 128), and 2^(j/256) - 1 as hi + lo
@@ -517,7 +519,8 @@ void localize(mwu_ctx* c) {
   if (c->kind == K_DOMSET) {
     // covering rows (vertices) by nnz-balanced ranges on even rows (16-byte aligned row slices)
     std::vector<int64_t> rp(c->nv + 1);
-    CK(cudaMemcpy(rp.data(), c->csrC.rowptr, (c->nv + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(rp.data(), c->csrC.rowptr, (c->nv + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
     for (int r = 1; r < c->world; ++r) {
       const int64_t target = (int64_t)((__int128)c->nnzC * r / c->world);
       int64_t row = std::lower_bound(rp.begin(), rp.end(), target) - rp.begin();
@@ -632,6 +635,40 @@ const double* unperm(mwu_ctx* c, const double* in, int w) {
   return c->tmp2;
 }
 
+// Propagation blocking for bmatch (MWU_PB=1): static per-bucket capacities from the dst-row
+// histogram of the local edges.
+void build_buckets(mwu_ctx* c) {
+  if (c->kind != K_MATCH || !c->scatterP || c->E <= 0) return;
+  const char* env = getenv("MWU_PB");
+  // off by default: with 128 buckets and degree-ordered rows the global bucket cursors are a
+  // contention point (c5 column 440 ms vs 65 ms direct); per-CTA slot chunks
+  // would be needed
+  const bool on = env ? atoi(env) != 0 : false;
+  if (!on) return;
+  const int shift = 20;
+  const int nb = (int)((c->mP + (1 << shift) - 1) >> shift);
+  unsigned long long* hist = talloc<unsigned long long>(nb + 1);
+  CK(cudaMemsetAsync(hist, 0, (nb + 1) * sizeof(unsigned long long), c->st));
+  k_bucket_hist<<<grid_for(c, c->E), MWU_NT, 0, c->st>>>(c->E, c->drow, shift, hist);
+  CKL();
+  std::vector<unsigned long long> h(nb);
+  CK(cudaMemcpyAsync(h.data(), hist, nb * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st));
+  sync(c);                                   // the context stream is non-blocking
+  tfree(hist);
+  std::vector<int64_t> base(nb + 1, 0);
+  for (int b = 0; b < nb; ++b) base[b + 1] = base[b] + (int64_t)h[b];
+  c->bkcap = base[nb];
+  int64_t* dbase = dalloc<int64_t>(c, nb + 1);
+  CK(cudaMemcpyAsync(dbase, base.data(), (nb + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->st));
+  sync(c);
+  c->bk.row = dalloc<int32_t>(c, c->bkcap);
+  c->bk.val = dalloc<double>(c, c->bkcap);
+  c->bk.base = dbase;
+  c->bk.cnt = dalloc<int32_t>(c, nb);
+  c->bk.shift = shift;
+  c->bk.nb = nb;
+}
+
 // ------------------------------------------------------------------------------ CSR build
 void copy_csr_checked(mwu_ctx* c, const mwu_csr* A, Seg& S, int64_t cols, const char* name) {
   if (A->rows < 0 || A->cols != cols || A->nnz < 0 || !A->rowptr || (A->nnz > 0 && !A->colidx))
@@ -722,10 +759,18 @@ void enqueue_column(mwu_ctx* c, cudaStream_t st) {
         CK(cudaMemsetAsync(c->dy, 0, (c->mP > 0 ? c->mP : 1) * sizeof(double), st));
         const int64_t blocks = (c->E + 2 * MWU_NT - 1) / (2 * MWU_NT);
         const int g = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, 3 * c->sms));
+        if (c->bk.row) CK(cudaMemsetAsync(c->bk.cnt, 0, c->bk.nb * sizeof(int32_t), st));
         col_match_fast<<<g, MWU_NT, 0, st>>>(c->E, c->srow, c->drow, c->u, c->x, c->d, c->dy,
                                             c->record ? c->gdbg : nullptr, c->record ? c->hdbg : nullptr,
-                                            c->ctl, c->part, c->counter);
+                                            c->ctl, c->part, c->counter, c->bk);
         c->launches++;
+        if (c->bk.row) {
+          const int gf = (int)std::max<int64_t>(1, std::min<int64_t>(4 * c->sms, (c->bkcap + MWU_NT - 1) / MWU_NT));
+          bucket_flush<<<gf, MWU_NT, (2 * c->bk.nb + 1) * sizeof(int64_t), st>>>(c->bkcap, c->bk.row, c->bk.val,
+                                                                              c->bk.base, c->bk.cnt, c->bk.nb,
+                                                                              c->dy, c->ctl);
+          c->launches++;
+        }
         break;
       }
       col_match<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, c->srow, c->drow, c->u, c->x, c->d,
@@ -1384,6 +1429,7 @@ mwu_status mwu_create_graph(const mwu_graph* g, const mwu_options* opt, mwu_ctx*
       throw MwuError{MWU_ERR_ARG, "multi-GPU sharding needs a graph kind with deterministic = 0"};
     localize(c);
     alloc_vectors(c);
+    build_buckets(c);
     {                                        // exchange flags for reductions before a probe
       Ctl& h = *c->hctl;
       memset(&h, 0, sizeof(Ctl));

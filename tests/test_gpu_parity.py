@@ -357,3 +357,17 @@ def test_host_buffers_e2e(cuda_ok):
     r = O.solve("bmatch", *G.numpy(), G.n_vertices, eps=0.1)
     assert S.stats()["objective"] == pytest.approx(r.objective, rel=1e-6)
     assert xh.device.type == "cpu"
+
+
+@pytest.mark.parametrize("kind,i", [("bmatch", 2), ("match", 1)])
+def test_bucketed_scatter_parity(cuda_ok, kind, i, monkeypatch):
+    """Propagation-blocked forward product (MWU_PB=1; off by default): the same
+    lockstep checks as the direct scatter."""
+    monkeypatch.setenv("MWU_PB", "1")
+    G = _graph(kind, i)
+    s, d = G.numpy()
+    B, _ = _oracle_probe_bound(kind, G)
+    lp = O.graph_lp(kind, s, d, G.n_vertices, B)
+    probe = O.Probe(lp, EPS[kind], max_iter=5000)
+    S = solver_for(kind, G)
+    lockstep(S, probe, B, EPS[kind], 50, alphas=None, window=self_sensitivity_window(lp, EPS[kind], None, 50))
