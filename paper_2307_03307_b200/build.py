@@ -5,7 +5,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SO = os.path.join(HERE, "libmwu.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("mwu.cu", "common.cuh", "kernels.cuh", "storage.cuh", "comm.cuh")]
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("mwu.cu", "common.cuh", "kernels.cuh", "storage.cuh", "comm.cuh", "fastmath.cuh")]
 HEADER = os.path.join(ROOT, "include", "mwu.h")
 
 NVCC_FLAGS = [

@@ -13,7 +13,9 @@
 #define MWU_NT 256            // threads per block for every kernel
 #define MWU_MAXC 8            // step-search candidates evaluated per HBM pass
 #define MWU_SLOTS 48          // reduction slots per block partial (6 * MAXC)
+#ifndef MWU_CT
 #define MWU_CT 1024           // edges per column tile (compacted covering-row records)
+#endif
 #define MWU_TILE 2048         // items per seg tile (a tile loads <= 2*TILE items into smem)
 #define MWU_LCH 8192          // items per chunk of a long row (deg > TILE)
 

@@ -50,10 +50,23 @@ static const double kMwuInvFact[13] = {
     0.5, 1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.0, 1.0 / 720.0, 1.0 / 5040.0, 1.0 / 40320.0, 1.0 / 362880.0,
     1.0 / 3628800.0, 1.0 / 39916800.0, 1.0 / 479001600.0, 1.0 / 6227020800.0, 1.0 / 87178291200.0};
 
-#if defined(__CUDA_ARCH__)
 #define MWU_IF(k) kMwuInvFact[k]
+
+// constants of the table-driven exp (device: constant bank operands instead of a pair of
+// uniform-register moves per 64-bit immediate and use)
+#if defined(__CUDACC__)
+__constant__ double kMwuTabC[8] = {
 #else
-#define MWU_IF(k) kMwuInvFact[k]
+static const double kMwuTabC[8] = {
+#endif
+    709.78, 369.3299304675746, 0.00270760617331689, 7.453964567463233e-13,
+    1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 8.673617379884035e-19};
+#if defined(__CUDA_ARCH__)
+#define MWU_TC(k) kMwuTabC[k]
+#else
+#define MWU_TC(k) (k == 0 ? 709.78 : k == 1 ? 369.3299304675746 : k == 2 ? 0.00270760617331689 \
+                   : k == 3 ? 7.453964567463233e-13 : k == 4 ? 1.0 / 120.0 : k == 5 ? 1.0 / 24.0 \
+                   : k == 6 ? 1.0 / 6.0 : 8.673617379884035e-19)
 #endif
 
 // p = expm1(r) for |r| <= ~0.35
@@ -144,21 +157,21 @@ MWU_HD void mwu_expm1_exp_tab(double x, const double* T, const double* Mh, const
 }
 MWU_HD double mwu_exp_tab(double x, const double* T) {
   if (!(x >= -745.5)) return 0.0;
-  if (x > 709.78) return INFINITY;
-  const double kd = rint(x * 369.3299304675746);              // 256 / ln2
-  double r = MWU_FMA(-kd, 0.00270760617331689, x);             // ln2/256 hi, 32 bits (exact product)
-  r = MWU_FMA(-kd, 7.453964567463233e-13, r);                 // ln2/256 lo
+  if (x > MWU_TC(0)) return INFINITY;
+  const double kd = rint(x * MWU_TC(1));                       // 256 / ln2
+  double r = MWU_FMA(-kd, MWU_TC(2), x);                       // ln2/256 hi, 32 bits (exact product)
+  r = MWU_FMA(-kd, MWU_TC(3), r);                              // ln2/256 lo
   const int ki = (int)kd;
   const int j = ki & 255, k = (ki - j) / 256;                  // kd = 256 k + j, 0 <= j < 256
-  double p = 1.0 / 120.0;
-  p = MWU_FMA(p, r, 1.0 / 24.0);
-  p = MWU_FMA(p, r, 1.0 / 6.0);
+  double p = MWU_TC(4);
+  p = MWU_FMA(p, r, MWU_TC(5));
+  p = MWU_FMA(p, r, MWU_TC(6));
   p = MWU_FMA(p, r, 0.5);
   p = MWU_FMA(p, r * r, r);                                    // expm1(r)
   const double t = T[j];
   const double m = MWU_FMA(t, p, t);                           // 2^(j/256) e^r
   if (k >= -1021) return m * mwu_pow2i(k);
-  return (m * mwu_pow2i(k + 60)) * 8.673617379884035e-19;
+  return (m * mwu_pow2i(k + 60)) * MWU_TC(7);
 }
 
 MWU_HD double mwu_exp(double x) {

@@ -1245,7 +1245,13 @@ __device__ __forceinline__ bool act_bit(const uint32_t* act, int e) { return (__
 #ifndef MWU_COL_DENSE_XD
 #define MWU_COL_DENSE_XD 0    // 1: stage x and d of every edge too (measured slower: 2 stages only)
 #endif
-constexpr int kColStages = MWU_COL_DENSE_XD ? 2 : 4;
+#ifndef MWU_COL_MINB
+#define MWU_COL_MINB 2        // resident column CTAs per SM (grid = MWU_COL_MINB x SMs)
+#endif
+#ifndef MWU_COL_STAGES
+#define MWU_COL_STAGES 4
+#endif
+constexpr int kColStages = MWU_COL_DENSE_XD ? 2 : MWU_COL_STAGES;
 constexpr int kColOffS = MWU_CT * 8, kColOffD = kColOffS + MWU_CT * 4, kColOffA = kColOffD + MWU_CT * 4;
 constexpr int kColOffX = ((kColOffA + (MWU_CT / 32) * 4) + 127) / 128 * 128;   // x pairs, then d pairs
 constexpr int kColOffDD = kColOffX + MWU_CT * 16;
@@ -1284,7 +1290,7 @@ __device__ __forceinline__ void col_gather(const char* stage, int rows, const do
   }
 }
 
-__global__ void __launch_bounds__(MWU_NT, 2) col_densest_fast(
+__global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
     int64_t E64, const int32_t* __restrict__ srow, const int32_t* __restrict__ drow, const double* __restrict__ u,
     double* __restrict__ x, double* __restrict__ d, double* __restrict__ z, double* __restrict__ dy,
     uint32_t* __restrict__ act, double* __restrict__ rz, double* __restrict__ rdz, double* __restrict__ rv,
@@ -1298,7 +1304,7 @@ __global__ void __launch_bounds__(MWU_NT, 2) col_densest_fast(
   const int apply = c->apply_prev;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int E = (int)E64;                  // the fast path requires E < 2^31 - MWU_CT (host check)
-  double maxd = -INFINITY;
+  double maxd = 0.0;                       // every d >= 0 and E > 0: max d >= 0 (inactive rows add 0)
   double im = INFINITY, is = 0.0;          // inactive rows: min z and sum of v (shift s_C)
   double2* x2 = reinterpret_cast<double2*>(x);
   double2* d2 = reinterpret_cast<double2*>(d);
@@ -1393,7 +1399,7 @@ __global__ void __launch_bounds__(MWU_NT, 2) col_densest_fast(
       const double dz = d0 + d1;
       const bool nz = dz > 0.0;
       if (nz) { d2[e] = make_double2(d0, d1); ++nact; const double m01 = d0 > d1 ? d0 : d1; maxd = m01 > maxd ? m01 : maxd; }
-      else if (valid) { im = zz < im ? zz : im; is += v; maxd = maxd > 0.0 ? maxd : 0.0; }   // candidate-independent row
+      else if (valid) { im = zz < im ? zz : im; is += v; }         // candidate-independent row
       zk[k] = zz; dzk[k] = dz; vk[k] = v;
       const uint32_t bw = __ballot_sync(0xffffffffu, nz);
       if (lane == 0 && valid && bw != pw[k]) act[e >> 5] = bw;

@@ -580,26 +580,13 @@ const double* gather_full(mwu_ctx* c, const double* local, int w) {
 // Fast edge-variable kinds: L2-blocked internal edge order (storage.cuh k_block_keys) and the
 // endpoint rows of the internal order.  perm maps internal -> original edge ids (Q29 order is
 // restored by every vector hook and mwu_get_x).
-constexpr int kBlockLDefault = 22, kBlockRDefault = 20;   // src blocks of 4M vertices, dst blocks of 1M
+constexpr int kBlockLDefault = 22, kBlockRDefault = 20;   // src blocks of 4M rows, dst blocks of 1M rows
 void build_blocked_order(mwu_ctx* c) {
   const int64_t E = c->E;
   if (E <= 0) return;
   const char* eL = getenv("MWU_BLOCK_L");      // experiment knobs
   const char* eR = getenv("MWU_BLOCK_R");
   const int kBlockL = eL ? atoi(eL) : kBlockLDefault, kBlockR = eR ? atoi(eR) : kBlockRDefault;
-  const int nbL = (int)((c->nv + (int64_t(1) << kBlockL) - 1) >> kBlockL);
-  const int nbR = (int)((c->nv + (int64_t(1) << kBlockR) - 1) >> kBlockR);
-  unsigned long long *keys = talloc<unsigned long long>(E), *kout = talloc<unsigned long long>(E);
-  uint32_t* vals = talloc<uint32_t>(E);
-  c->perm = dalloc<uint32_t>(c, E);
-  k_block_keys<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->src, c->dst, nbR, kBlockL, kBlockR, keys, vals);
-  CKL();
-  int bits = kBlockL + kBlockR;
-  while (bits < 64 && (1ull << (bits - kBlockL - kBlockR)) < (unsigned long long)nbL * (unsigned long long)nbR) ++bits;
-  size_t tb = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, kout, vals, c->perm, E, 0, bits, c->st));
-  void* t = talloc<char>(tb);
-  CK(cub::DeviceRadixSort::SortPairs(t, tb, keys, kout, vals, c->perm, E, 0, bits, c->st));
   // packing rows in degree-descending order (fast path only; hooks restore vertex order)
   int32_t* prowf = talloc<int32_t>(c->nv);
   {
@@ -617,12 +604,26 @@ void build_blocked_order(mwu_ctx* c) {
     sync(c);
     tfree(t2); tfree(dk); tfree(dko); tfree(dv); tfree(dvo);
   }
+  // L2 blocks over ROW ranges of the (degree-ordered) packing-row vectors: key = (srow >> BL,
+  // drow >> BR, srow, drow)
+  const int64_t nr = std::max<int64_t>(c->nprime, 1);
+  const int nbL = (int)((nr + (int64_t(1) << kBlockL) - 1) >> kBlockL);
+  const int nbR = (int)((nr + (int64_t(1) << kBlockR) - 1) >> kBlockR);
+  unsigned long long *keys = talloc<unsigned long long>(E), *kout = talloc<unsigned long long>(E);
+  uint32_t* vals = talloc<uint32_t>(E);
+  c->perm = dalloc<uint32_t>(c, E);
+  k_block_keys<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->src, c->dst, prowf, nbR, kBlockL, kBlockR, keys, vals);
+  CKL();
+  int bits = kBlockL + kBlockR;
+  while (bits < 64 && (1ull << (bits - kBlockL - kBlockR)) < (unsigned long long)nbL * (unsigned long long)nbR) ++bits;
+  size_t tb = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, kout, vals, c->perm, E, 0, bits, c->st));
+  void* t = talloc<char>(tb);
+  CK(cub::DeviceRadixSort::SortPairs(t, tb, keys, kout, vals, c->perm, E, 0, bits, c->st));
   k_map_endpoints_perm<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->perm, c->src, c->dst, prowf, c->srow, c->drow);
   CKL();
   sync(c);
   tfree(prowf);
-  CKL();
-  sync(c);
   tfree(t); tfree(keys); tfree(kout); tfree(vals);
 }
 
@@ -782,7 +783,7 @@ void enqueue_column(mwu_ctx* c, cudaStream_t st) {
       if (c->lazyC) {
         CK(cudaMemsetAsync(c->dy, 0, (c->mP > 0 ? c->mP : 1) * sizeof(double), st));
         const int64_t nt = c->ntilesC;
-        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(nt, 2 * c->sms));
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(nt, MWU_COL_MINB * c->sms));
         col_densest_fast<<<g, MWU_NT, kColSmem, st>>>(c->E, c->srow, c->drow, c->u, c->x, c->d, c->z, c->dy, c->act, c->rz,
                                               c->rdz, c->rv, c->tcnt, c->record ? c->gdbg : nullptr,
                                               c->record ? c->hdbg : nullptr, c->ctl, c->part, c->counter, c->exptab);

@@ -107,11 +107,12 @@ __global__ void k_map_endpoints(int64_t E, const int32_t* src, const int32_t* ds
 // L2-resident (its gathered u and scattered d^(y) slices) while the narrow dst blocks (2^BR)
 // stream past it, so each random-access slice is fetched ~once per src block instead of once
 // per access.
-__global__ void k_block_keys(int64_t E, const int32_t* src, const int32_t* dst, int nbR, int BL, int BR,
-                             unsigned long long* keys, uint32_t* vals) {
+// vrow: vertex -> packing row (the blocks are row ranges of the gathered / scattered vectors)
+__global__ void k_block_keys(int64_t E, const int32_t* src, const int32_t* dst, const int32_t* vrow, int nbR,
+                             int BL, int BR, unsigned long long* keys, uint32_t* vals) {
   const unsigned long long mL = (1ull << BL) - 1ull, mR = (1ull << BR) - 1ull;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
-    const unsigned long long a = (unsigned long long)src[e], b = (unsigned long long)dst[e];
+    const unsigned long long a = (unsigned long long)vrow[src[e]], b = (unsigned long long)vrow[dst[e]];
     const unsigned long long pair = (a >> BL) * (unsigned long long)nbR + (b >> BR);
     keys[e] = (pair << (BL + BR)) | ((a & mL) << BR) | (b & mR);
     vals[e] = (uint32_t)e;
