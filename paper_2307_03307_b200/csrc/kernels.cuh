@@ -1061,7 +1061,10 @@ __device__ __forceinline__ void search_body_gen(const SearchArgs& A, const Cands
 
 // One HBM pass evaluating the staged candidates (P:716-727 on cached vectors); the
 // last block replays Alg. 3 (search_controller).
-__global__ void __launch_bounds__(MWU_NT, 2) search_pass(SearchArgs A, Ctl* c, double* part, unsigned int* counter) {
+#ifndef MWU_SEARCH_MINB
+#define MWU_SEARCH_MINB 2     // resident search CTAs per SM (grid = MWU_SEARCH_MINB x SMs)
+#endif
+__global__ void __launch_bounds__(MWU_NT, MWU_SEARCH_MINB) search_pass(SearchArgs A, Ctl* c, double* part, unsigned int* counter) {
   if (c->status != ST_RUNNING || !c->sactive) {
     if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(c->h_search, 0u);
     return;
@@ -1238,7 +1241,7 @@ __device__ __forceinline__ void red_add_f64(double* p, double v) {
 // kernel reads x and d, and writes x, z and d, only for edges active in this or the last step.
 __device__ __forceinline__ bool act_bit(const uint32_t* act, int e) { return (__ldg(act + (e >> 5)) >> (e & 31)) & 1u; }
 
-// The per-edge stream of each 512-edge tile (z, src/dst rows, activity words) is staged into
+// The per-edge stream of each 1024-edge tile (z, src/dst rows, activity words) is staged into
 // shared memory by the bulk-copy engine (cp.async.bulk + mbarrier) kColStages tiles ahead; the
 // u gathers of tile i+1 are issued (registers) before tile i is computed.  Stages are released per warp (an 8-arrival "empty" mbarrier), so
 // only the producer thread waits for the slowest warp; no block-wide barrier in the loop.

@@ -905,7 +905,7 @@ void enqueue_forward(mwu_ctx* c, cudaStream_t st, const double* in, double* oy, 
 
 void enqueue_search(mwu_ctx* c, cudaStream_t st) {
   const int64_t chunks = (std::max(c->mP, c->mC) + MWU_SCH - 1) / MWU_SCH;
-  const int g = (int)std::max<int64_t>(1, std::min<int64_t>(2 * c->sms, chunks));   // 2 CTAs / SM
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>(MWU_SEARCH_MINB * c->sms, chunks));
   SearchArgs A;
   int64_t p0 = 0, p1 = c->mP;                // sharded: each rank sums a slice of the replicated rows
   if (c->sharded) {

@@ -158,10 +158,13 @@ def test_sharded_solve(cuda_ok, ci):
     runs = [O.solve(kind, s, d, G.n_vertices, eps=eps, max_iter=400, x0_scale=sc)
             for sc in (1.0, 1 + 2.0 ** -52, 1 - 2.0 ** -52)]
     if kind in ("vcover", "domset"):
-        # pure covering: the bisection's bound is the reproducible result; <1, x_out> depends
-        # on the (chaotic) final iterate even for the oracle's own one-ulp reruns
+        # pure covering: the sharded covering kinds run only on the fast path, whose fp64
+        # reductions (red.add into the column gradient) have no fixed order, so a probe near the
+        # feasibility threshold may flip its verdict: the bound is reproducible only to the outer
+        # bisection's bracket (eps/4 relative) per side; <1, x_out> depends on the
+        # (chaotic) final iterate even for the oracle's own one-ulp reruns
         refs = [st1["bound"]] + [q.bound for q in runs]
-        assert any(abs(st0["bound"] - q) <= 1e-6 * abs(q) for q in refs), (st0["bound"], refs)
+        assert any(abs(st0["bound"] - q) <= 0.5 * eps * abs(q) for q in refs), (st0["bound"], refs)
         assert abs(st0["objective"] - st1["objective"]) <= eps * st1["objective"]
     else:
         refs = [st1["objective"]] + [q.objective for q in runs]
