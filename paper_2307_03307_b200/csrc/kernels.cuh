@@ -1346,7 +1346,6 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
     const int32_t* ssr = reinterpret_cast<const int32_t*>(stg + kColOffS);
     const int32_t* sdr = reinterpret_cast<const int32_t*>(stg + kColOffD);
     const uint32_t* sac = reinterpret_cast<const uint32_t*>(stg + kColOffA);
-    double zk[kColEdges], dzk[kColEdges], vk[kColEdges];
     double2 xe[kColEdges], dp[kColEdges];
     bool had[kColEdges];
     uint32_t pw[kColEdges];
@@ -1362,7 +1361,10 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
         }
       } else if (had[k]) { xe[k] = x2[e0 + j]; dp[k] = d2[e0 + j]; }
     }
-    int nact = 0;
+    // compaction of the active covering rows: each warp owns the record segment
+    // [tile*CT + warp*kWarpSeg, +kWarpSeg) of its kWarpSeg edges, filled in (k, lane) order
+    const int seg0 = tile * MWU_CT + warp * kWarpSeg;
+    int wp = seg0;
 #pragma unroll
     for (int k = 0; k < kColEdges; ++k) {
       const int j = k * MWU_NT + threadIdx.x;
@@ -1401,10 +1403,15 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
       }
       const double dz = d0 + d1;
       const bool nz = dz > 0.0;
-      if (nz) { d2[e] = make_double2(d0, d1); ++nact; const double m01 = d0 > d1 ? d0 : d1; maxd = m01 > maxd ? m01 : maxd; }
-      else if (valid) { im = zz < im ? zz : im; is += v; }         // candidate-independent row
-      zk[k] = zz; dzk[k] = dz; vk[k] = v;
       const uint32_t bw = __ballot_sync(0xffffffffu, nz);
+      if (nz) {
+        d2[e] = make_double2(d0, d1);
+        const double m01 = d0 > d1 ? d0 : d1;
+        maxd = m01 > maxd ? m01 : maxd;
+        const int p = wp + __popc(bw & ((1u << lane) - 1u));
+        rz[p] = zz; rdz[p] = dz; rv[p] = v;
+      } else if (valid) { im = zz < im ? zz : im; is += v; }       // candidate-independent row
+      wp += __popc(bw);
       if (lane == 0 && valid && bw != pw[k]) act[e >> 5] = bw;
 #if MWU_ABLATE != 3
       if (d1 > 0.0) red_add_f64(dy + dr, invD * d1);              // dst side: random rows
@@ -1419,19 +1426,7 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
     // this warp is done with the stage: release it
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
-    // compaction of the active covering rows: each warp owns the record segment
-    // [tile*CT + warp*kWarpSeg, +kWarpSeg) of its kWarpSeg edges
-    int incl = nact;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
-    }
-    int p = tile * MWU_CT + warp * kWarpSeg + incl - nact;
-#pragma unroll
-    for (int k = 0; k < kColEdges; ++k)
-      if (dzk[k] > 0.0) { rz[p] = zk[k]; rdz[p] = dzk[k]; rv[p] = vk[k]; ++p; }
-    if (lane == 31) tcnt[tile * (MWU_NT / 32) + warp] = incl;
+    if (lane == 0) tcnt[tile * (MWU_NT / 32) + warp] = wp - seg0;
     if (threadIdx.x == 0 && kt + kColStages < mine) {           // producer: refill once all warps left
       mbar_wait(&empty[slot], (uint32_t)((kt / kColStages) & 1));
       col_issue(stg, &full[slot], blockIdx.x + (kt + kColStages) * gridDim.x, E, z, srow, drow, act, x, d);
