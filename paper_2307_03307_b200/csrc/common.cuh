@@ -48,6 +48,8 @@ enum Action : int {
   A_SUM = 9,        // generic: store the reduced slots in ctl->scratch
   A_COL_FAST = 10,  // fast densest column: max d, inactive covering aggregate (mzi, Vi)
   A_VI_EXACT = 11,  // exact inactive aggregate at shift mzi (rare path)
+  A_STEP_DONE_C = 12,  // vcover forward product with compacted covering records: inactive
+                       // aggregate (mzi, Vi), then as A_STEP_DONE
 };
 
 // Device-resident control block of one probe (one per context).
@@ -58,7 +60,7 @@ struct Ctl {
   int32_t pSing, cSing;                // side is the embedded singleton row
   int32_t mode;                        // 0 mixed, 1 pure packing, 2 pure covering
   int32_t tol_prose, max_evals, bisect_depth, use_graph;
-  int32_t lazyC, pad0_;                // covering rows of the fast densest path: z updated lazily in
+  int32_t lazyC, compC;                 // covering rows of the fast densest path: z updated lazily in
                                        // the column kernel, weights v recomputed from z, S_C carried
                                        // from the accepted alpha's search pass
   // ---- iteration state

@@ -324,6 +324,15 @@ __device__ void finalize(Ctl* c, int action, double* r) {
     case A_STEP_MAXDY:
       c->maxdy = r[0];
       break;
+    case A_STEP_DONE_C:
+      // r = (max d^(z), min z, sum v) over the rows with d^(z) = 0; v is stored at shift s_C,
+      // the aggregate is carried at shift mzi (exact pass when terms may have underflowed)
+      c->mzi = r[1];
+      c->vi_exact = 0;
+      if (!(r[2] > 0.0)) c->Vi = 0.0;
+      else if (c->eta * (c->mzi - c->sC) <= 600.0) c->Vi = r[2] * exp(c->eta * (c->mzi - c->sC));
+      else c->vi_exact = 1;
+      // fall through
     case A_STEP_DONE:
     case A_STEP_DONE + 100: {
       if (action == A_STEP_DONE + 100) c->maxdy = r[0];
@@ -341,7 +350,7 @@ __device__ void finalize(Ctl* c, int action, double* r) {
       break;
     }
     case A_SEARCH:
-      if (c->lazyC) {
+      if (c->lazyC || c->compC) {
         // covering rows with d^(z) = 0 were not streamed: they add exp(-eta(z - shC)) to the
         // shifted sums and z to the minima, for every candidate alike
         for (int j = 0; j < c->ncand; ++j) {
@@ -750,6 +759,76 @@ __global__ void __launch_bounds__(MWU_NT) edge_sum(int64_t E, const int32_t* __r
   }
   const int ops[1] = {OP_MAX};
   reduce_and_finalize<1>(acc, ops, part, counter, c, action);
+}
+
+// VCOVER forward product d^(z) = M^T d (edge rows) fused with the compaction of the
+// covering rows with d^(z) > 0 into per-warp records (z, d^(z), v) — the layout of the fast
+// densest column kernel — and the candidate-independent aggregate (min z, sum v) of the others,
+// so the search passes stream only the active rows.
+__global__ void __launch_bounds__(MWU_NT) edge_sum_compact(int64_t E64, const int32_t* __restrict__ src,
+                                                           const int32_t* __restrict__ dst,
+                                                           const double* __restrict__ in, double* __restrict__ out,
+                                                           const double* __restrict__ z, const double* __restrict__ v,
+                                                           double* __restrict__ rz, double* __restrict__ rdz,
+                                                           double* __restrict__ rv, int32_t* __restrict__ tcnt, Ctl* c,
+                                                           double* part, unsigned int* counter) {
+  if (c->status != ST_RUNNING) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(c->h_search, 0u);
+    return;
+  }
+  const int E = (int)E64;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ntiles = (E + MWU_CT - 1) / MWU_CT;
+  double acc[3] = {-INFINITY, INFINITY, 0.0};
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int seg0 = tile * MWU_CT + warp * kWarpSeg;
+    int wp = seg0;
+    double s[kColEdges], zz[kColEdges], vv[kColEdges];
+#pragma unroll
+    for (int k = 0; k < kColEdges; ++k) {
+      const int e = tile * MWU_CT + k * MWU_NT + threadIdx.x;
+      if (e < E) {
+        s[k] = __ldg(in + __ldcs(src + e)) + __ldg(in + __ldcs(dst + e));
+        zz[k] = __ldcs(z + e); vv[k] = __ldcs(v + e);
+      } else {
+        s[k] = 0.0; zz[k] = INFINITY; vv[k] = 0.0;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kColEdges; ++k) {
+      const int e = tile * MWU_CT + k * MWU_NT + threadIdx.x;
+      const bool nz = s[k] > 0.0;
+      const uint32_t bw = __ballot_sync(0xffffffffu, nz);
+      if (e < E) {
+        out[e] = s[k];
+        acc[0] = fmax(acc[0], s[k]);
+        if (nz) {
+          const int p = wp + __popc(bw & ((1u << lane) - 1u));
+          rz[p] = zz[k]; rdz[p] = s[k]; rv[p] = vv[k];
+        } else {
+          acc[1] = fmin(acc[1], zz[k]);
+          acc[2] += vv[k];
+        }
+      }
+      wp += __popc(bw);
+    }
+    if (lane == 0) tcnt[tile * (MWU_NT / 32) + warp] = wp - seg0;
+  }
+  const int ops[3] = {OP_MAX, OP_MIN, OP_SUM};
+  reduce_and_finalize<3>(acc, ops, part, counter, c, A_STEP_DONE_C);
+}
+
+// Rare path of the vcover inactive aggregate (rows with d^(z) = 0), exactly at shift mzi.
+__global__ void __launch_bounds__(MWU_NT) inactive_exact_dz(int64_t E, const double* __restrict__ dz,
+                                                            const double* __restrict__ z, Ctl* c, double* part,
+                                                            unsigned int* counter) {
+  if (c->status != ST_RUNNING || !c->vi_exact) return;
+  const double neta = -c->eta, m = c->mzi;
+  double acc[1] = {0.0};
+  for (int64_t e = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; e < E; e += (int64_t)gridDim.x * MWU_NT)
+    if (!(dz[e] > 0.0)) acc[0] += exp(neta * (z[e] - m));
+  const int ops[1] = {OP_SUM};
+  reduce_and_finalize<1>(acc, ops, part, counter, c, A_VI_EXACT);
 }
 
 // DENSEST init: z_e = x_2e + x_2e+1 (W x).

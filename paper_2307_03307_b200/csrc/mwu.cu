@@ -82,6 +82,7 @@ struct mwu_ctx {
   uint32_t* rowperm = nullptr;  // scatterP: fast (degree-ordered) packing row -> vertex-order row
   Buckets bk{};                 // bmatch with an out-of-L2 packing side: propagation blocking
   int64_t bkcap = 0;
+  int compC = 0;             // vcover (fast, one rank): forward product writes compacted covering records
   int fastC = 0;             // vcover / domset: transposed (and domset forward) products scattered
   double* exptab = nullptr;  // 2^(j/256), j < 256 (fastmath.cuh mwu_exp_tab)
   double* emtab = nullptr;   // 2^(j/256), j in [-128, 128), and 2^(j/256) - 1 as hi + lo
@@ -279,12 +280,14 @@ void alloc_vectors(mwu_ctx* c) {
   c->dy = dalloc<double>(c, c->mP);
   c->u = dalloc<double>(c, c->mP);
   c->z = dalloc<double>(c, c->mC);
-  if (c->lazyC) {
+  if (c->lazyC || c->compC) {
     c->ntilesC = (c->E + MWU_CT - 1) / MWU_CT;
     c->rz = dalloc<double>(c, c->ntilesC * MWU_CT);
     c->rdz = dalloc<double>(c, c->ntilesC * MWU_CT);
     c->rv = dalloc<double>(c, c->ntilesC * MWU_CT);
     c->tcnt = dalloc<int32_t>(c, c->ntilesC * (MWU_NT / 32));
+  }
+  if (c->lazyC) {
     c->act = dalloc<uint32_t>(c, c->ntilesC * (MWU_CT / 32));
     CK(cudaMemsetAsync(c->act, 0, c->ntilesC * (MWU_CT / 32) * sizeof(uint32_t), c->st));
   } else {
@@ -581,6 +584,12 @@ const double* gather_full(mwu_ctx* c, const double* local, int w) {
 // endpoint rows of the internal order.  perm maps internal -> original edge ids (Q29 order is
 // restored by every vector hook and mwu_get_x).
 constexpr int kBlockLDefault = 22, kBlockRDefault = 20;   // src blocks of 4M rows, dst blocks of 1M rows
+// env knob: NAME=0 turns a default-on fast-path feature off (experiments / A-B runs)
+bool getenv_flag_off(const char* name) {
+  const char* e = getenv(name);
+  return e && atoi(e) == 0;
+}
+
 void build_blocked_order(mwu_ctx* c) {
   const int64_t E = c->E;
   if (E <= 0) return;
@@ -875,6 +884,14 @@ void enqueue_forward(mwu_ctx* c, cudaStream_t st, const double* in, double* oy, 
       launch_seg(c, st, c->inc_p, item_of(c->inc_p, in, 0, invB), ey, a_done_p);
       break;
     case K_VCOVER:
+      if (!init && c->compC) {
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(c->ntilesC, 4 * c->sms));
+        edge_sum_compact<<<g, MWU_NT, 0, st>>>(c->E, c->src, c->dst, in, oz, c->z, c->v, c->rz, c->rdz, c->rv,
+                                               c->tcnt, c->ctl, c->part, c->counter);
+        inactive_exact_dz<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, oz, c->z, c->ctl, c->part, c->counter);
+        c->launches += 2;
+        break;
+      }
       edge_sum<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, c->src, c->dst, in, oz, c->ctl, c->part, c->counter, a_done);
       c->launches++;
       break;
@@ -1008,6 +1025,7 @@ void probe_begin(mwu_ctx* c, double bound, double eps) {
   h.bisect_depth = c->opt.bisect_depth;
   h.use_graph = c->opt.use_graph;
   h.lazyC = c->lazyC;
+  h.compC = c->compC;
   h.world = c->sharded ? std::max(2, c->world) : 1;   // device: defer partial reductions when sharded
   h.repvars = c->fastC ? 1 : 0;                          // covering kinds: variables replicated
   h.partupd = (c->sharded && c->fastC) ? 1 : 0;          // their covering rows are local
@@ -1429,6 +1447,10 @@ mwu_status mwu_create_graph(const mwu_graph* g, const mwu_options* opt, mwu_ctx*
     if (c->sharded && !c->scatterP && !c->fastC)
       throw MwuError{MWU_ERR_ARG, "multi-GPU sharding needs a graph kind with deterministic = 0"};
     localize(c);
+    // vcover, one rank: the forward product compacts the covering rows with d^(z) > 0 for the
+    // search passes (sharded runs keep the dense rows: their step reductions are not exchanged)
+    c->compC = (c->kind == K_VCOVER && c->fastC && !c->sharded && c->E > 0 &&
+                c->E < (int64_t(1) << 31) - MWU_CT && !getenv_flag_off("MWU_COMPC")) ? 1 : 0;
     alloc_vectors(c);
     build_buckets(c);
     {                                        // exchange flags for reductions before a probe
