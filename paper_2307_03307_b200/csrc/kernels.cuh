@@ -764,7 +764,8 @@ __global__ void __launch_bounds__(MWU_NT) edge_sum(int64_t E, const int32_t* __r
 // VCOVER forward product d^(z) = M^T d (edge rows) fused with the compaction of the
 // covering rows with d^(z) > 0 into per-warp records (z, d^(z), v) — the layout of the fast
 // densest column kernel — and the candidate-independent aggregate (min z, sum v) of the others,
-// so the search passes stream only the active rows.
+// so the search passes stream only the active rows.  src == nullptr: d^(z) is
+// already in `in` (domset: scattered by csr_scatter); only the compaction runs.
 __global__ void __launch_bounds__(MWU_NT) edge_sum_compact(int64_t E64, const int32_t* __restrict__ src,
                                                            const int32_t* __restrict__ dst,
                                                            const double* __restrict__ in, double* __restrict__ out,
@@ -788,7 +789,7 @@ __global__ void __launch_bounds__(MWU_NT) edge_sum_compact(int64_t E64, const in
     for (int k = 0; k < kColEdges; ++k) {
       const int e = tile * MWU_CT + k * MWU_NT + threadIdx.x;
       if (e < E) {
-        s[k] = __ldg(in + __ldcs(src + e)) + __ldg(in + __ldcs(dst + e));
+        s[k] = src ? __ldg(in + __ldcs(src + e)) + __ldg(in + __ldcs(dst + e)) : __ldcs(in + e);
         zz[k] = __ldcs(z + e); vv[k] = __ldcs(v + e);
       } else {
         s[k] = 0.0; zz[k] = INFINITY; vv[k] = 0.0;
@@ -800,7 +801,7 @@ __global__ void __launch_bounds__(MWU_NT) edge_sum_compact(int64_t E64, const in
       const bool nz = s[k] > 0.0;
       const uint32_t bw = __ballot_sync(0xffffffffu, nz);
       if (e < E) {
-        out[e] = s[k];
+        if (src) out[e] = s[k];
         acc[0] = fmax(acc[0], s[k]);
         if (nz) {
           const int p = wp + __popc(bw & ((1u << lane) - 1u));

@@ -281,7 +281,7 @@ void alloc_vectors(mwu_ctx* c) {
   c->u = dalloc<double>(c, c->mP);
   c->z = dalloc<double>(c, c->mC);
   if (c->lazyC || c->compC) {
-    c->ntilesC = (c->E + MWU_CT - 1) / MWU_CT;
+    c->ntilesC = (c->mC + MWU_CT - 1) / MWU_CT;
     c->rz = dalloc<double>(c, c->ntilesC * MWU_CT);
     c->rdz = dalloc<double>(c, c->ntilesC * MWU_CT);
     c->rv = dalloc<double>(c, c->ntilesC * MWU_CT);
@@ -902,7 +902,16 @@ void enqueue_forward(mwu_ctx* c, cudaStream_t st, const double* in, double* oy, 
         csr_scatter<<<(int)std::min<int64_t>(4 * c->sms, (nz + 4 * MWU_NT - 1) / (4 * MWU_NT) + 1), MWU_NT, 0, st>>>(
             nz, c->rowidC + c->k0, c->csrC.idx + c->k0, in, oz, c->ctl, c->r0);
         c->launches++;
-        if (!init) { step_done<<<1, 32, 0, st>>>(c->ctl); c->launches++; }
+        if (!init && c->compC) {
+          const int g = (int)std::max<int64_t>(1, std::min<int64_t>(c->ntilesC, 4 * c->sms));
+          edge_sum_compact<<<g, MWU_NT, 0, st>>>(c->mC, nullptr, nullptr, oz, oz, c->z, c->v, c->rz, c->rdz, c->rv,
+                                                 c->tcnt, c->ctl, c->part, c->counter);
+          inactive_exact_dz<<<rows_grid(c, c->mC), MWU_NT, 0, st>>>(c->mC, oz, c->z, c->ctl, c->part, c->counter);
+          c->launches += 2;
+        } else if (!init) {
+          step_done<<<1, 32, 0, st>>>(c->ctl);
+          c->launches++;
+        }
         break;
       }
       launch_seg(c, st, c->csrC, item_of(c->csrC, in, 0, nullptr), ez, a_done);
@@ -1447,10 +1456,10 @@ mwu_status mwu_create_graph(const mwu_graph* g, const mwu_options* opt, mwu_ctx*
     if (c->sharded && !c->scatterP && !c->fastC)
       throw MwuError{MWU_ERR_ARG, "multi-GPU sharding needs a graph kind with deterministic = 0"};
     localize(c);
-    // vcover, one rank: the forward product compacts the covering rows with d^(z) > 0 for the
-    // search passes (sharded runs keep the dense rows: their step reductions are not exchanged)
-    c->compC = (c->kind == K_VCOVER && c->fastC && !c->sharded && c->E > 0 &&
-                c->E < (int64_t(1) << 31) - MWU_CT && !getenv_flag_off("MWU_COMPC")) ? 1 : 0;
+    // vcover / domset, one rank: the forward product compacts the covering rows with d^(z) > 0
+    // for the search passes (sharded runs keep the dense rows: their step reductions are not exchanged)
+    c->compC = ((c->kind == K_VCOVER || c->kind == K_DOMSET) && c->fastC && !c->sharded && c->mC > 0 &&
+                c->mC < (int64_t(1) << 31) - MWU_CT && !getenv_flag_off("MWU_COMPC")) ? 1 : 0;
     alloc_vectors(c);
     build_buckets(c);
     {                                        // exchange flags for reductions before a probe
