@@ -50,7 +50,15 @@ static const double kMwuInvFact[13] = {
     0.5, 1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.0, 1.0 / 720.0, 1.0 / 5040.0, 1.0 / 40320.0, 1.0 / 362880.0,
     1.0 / 3628800.0, 1.0 / 39916800.0, 1.0 / 479001600.0, 1.0 / 6227020800.0, 1.0 / 87178291200.0};
 
+#if defined(__CUDACC__) && !defined(__CUDA_ARCH__)
+// host pass of nvcc: the __constant__ array is device memory; read a host copy
+static const double kMwuInvFactH[13] = {
+    0.5, 1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.0, 1.0 / 720.0, 1.0 / 5040.0, 1.0 / 40320.0, 1.0 / 362880.0,
+    1.0 / 3628800.0, 1.0 / 39916800.0, 1.0 / 479001600.0, 1.0 / 6227020800.0, 1.0 / 87178291200.0};
+#define MWU_IF(k) kMwuInvFactH[k]
+#else
 #define MWU_IF(k) kMwuInvFact[k]
+#endif
 
 // constants of the table-driven exp (device: constant bank operands instead of a pair of
 // uniform-register moves per 64-bit immediate and use)

@@ -371,3 +371,20 @@ def test_bucketed_scatter_parity(cuda_ok, kind, i, monkeypatch):
     probe = O.Probe(lp, EPS[kind], max_iter=5000)
     S = solver_for(kind, G)
     lockstep(S, probe, B, EPS[kind], 50, alphas=None, window=self_sensitivity_window(lp, EPS[kind], None, 50))
+
+
+@pytest.mark.parametrize("kind", ["vcover", "domset"])
+@pytest.mark.parametrize("compc", ["0", "1"])
+def test_compact_covering_rows_parity(cuda_ok, kind, compc, monkeypatch):
+    """The search over compacted covering records plus the inactive aggregate (default for
+    vcover / domset on one rank) and over the dense rows (MWU_COMPC=0): both under
+    the lockstep checks against the oracle, on both graphs of the kind."""
+    monkeypatch.setenv("MWU_COMPC", compc)
+    for i in (0, 1):
+        G = _graph(kind, i)
+        s, d = G.numpy()
+        B, _ = _oracle_probe_bound(kind, G)
+        lp = O.graph_lp(kind, s, d, G.n_vertices, B)
+        probe = O.Probe(lp, EPS[kind], max_iter=5000)
+        S = solver_for(kind, G)
+        lockstep(S, probe, B, EPS[kind], 50, alphas=None, window=self_sensitivity_window(lp, EPS[kind], None, 50))
