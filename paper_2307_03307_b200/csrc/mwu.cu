@@ -71,6 +71,7 @@ struct mwu_ctx {
   // graph storage
   int32_t *src = nullptr, *dst = nullptr, *srow = nullptr, *drow = nullptr, *deg = nullptr, *prow = nullptr;
   Seg inc_all, inc_p;
+  int inc_fast = 0;          // fast edge-variable path: incidence rowptrs only (no slot list / plan)
   int64_t maxdeg = 0, nprime = 0;
   // CSR storage
   Seg csrP, cscP, csrC, cscC;
@@ -426,8 +427,13 @@ void build_graph_storage(mwu_ctx* c, const mwu_graph* g) {
       c->inc_p.nnz = 2 * E;
       c->inc_p.rowptr = dalloc<int64_t>(c, c->nprime + 1);
     }
+    // the fast path of the edge-variable kinds (d^(y) scattered by the column kernel over the
+    // blocked edge order) never walks the vertex -> slot incidence: skip its 2E-slot sort
+    const bool fastE = !c->opt.deterministic &&
+                       (g->kind == MWU_G_MATCH || g->kind == MWU_G_BMATCH ||
+                        (g->kind == MWU_G_DENSEST && E < (int64_t(1) << 31) - MWU_CT));
     // slots sorted by vertex (stable radix sort keeps slot order within a vertex)
-    if (g->kind != MWU_G_DOMSET) {
+    if (g->kind != MWU_G_DOMSET && !fastE) {
       c->inc_all.idx = dalloc<uint32_t>(c, 2 * E);
       if (E > 0) {
         uint32_t *keys = talloc<uint32_t>(2 * E), *kout = talloc<uint32_t>(2 * E), *vals = talloc<uint32_t>(2 * E);
@@ -449,8 +455,12 @@ void build_graph_storage(mwu_ctx* c, const mwu_graph* g) {
       c->inc_p.idx = c->inc_all.idx;
       c->srow = dalloc<int32_t>(c, E);
       c->drow = dalloc<int32_t>(c, E);
-      if (E > 0) { k_map_endpoints<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->src, c->dst, c->prow, c->srow, c->drow); CKL(); }
+      if (E > 0 && !fastE) {                  // fast path: written in the blocked order later
+        k_map_endpoints<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->src, c->dst, c->prow, c->srow, c->drow);
+        CKL();
+      }
       sync(c);
+      c->inc_fast = fastE ? 1 : 0;
     }
     sync(c);
     tfree(deg64); tfree(outm); tfree(fl); tfree(scan);
@@ -481,7 +491,7 @@ void build_graph_storage(mwu_ctx* c, const mwu_graph* g) {
     c->cscC = c->csrC;  // symmetric: the CSR doubles as the CSC (column side)
     c->nnzC = tot;
   }
-  if (c->inc_p.rowptr) build_plan(c, c->inc_p);
+  if (c->inc_p.rowptr && !c->inc_fast) build_plan(c, c->inc_p);
   if (g->kind == MWU_G_VCOVER) build_plan(c, c->inc_all);
 }
 

@@ -11,6 +11,7 @@ import torch
 
 import graphgen as gg
 import oracle as O
+from paper_2307_03307_b200.mwu import MwuError
 from gpu_common import (assert_vec, csr_tuple, lockstep, lp_mats, self_sensitivity_window, solver_for)
 
 pytestmark = pytest.mark.gpu
@@ -58,6 +59,12 @@ def test_structure_bit_exact(cuda_ok, kind, i):
         assert np.array_equal(S.structure("c_rowptr").numpy(), C.indptr.astype(np.int64))
         assert np.array_equal(S.structure("c_colidx").numpy(), C.indices.astype(np.int32))
         return
+    if kind in ("bmatch", "match", "densest"):
+        # the default (scattered, blocked-order) path builds no vertex -> slot list; the
+        # fixed-order engine does
+        with pytest.raises(MwuError):
+            S.structure("inc_slots")
+        S = solver_for(kind, G, deterministic=1)
     rp = S.structure("inc_rowptr").numpy()
     slots = S.structure("inc_slots").numpy().astype(np.uint32)
     assert np.array_equal(rp, M.indptr.astype(np.int64))
