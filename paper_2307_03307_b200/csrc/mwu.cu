@@ -605,7 +605,15 @@ void build_blocked_order(mwu_ctx* c) {
   if (E <= 0) return;
   const char* eL = getenv("MWU_BLOCK_L");      // experiment knobs
   const char* eR = getenv("MWU_BLOCK_R");
-  const int kBlockL = eL ? atoi(eL) : kBlockLDefault, kBlockR = eR ? atoi(eR) : kBlockRDefault;
+  // matching (random bipartite, degree ~16: no src-block reuse): one source block
+  // (edges sorted by src row) and 4M-row destination blocks whose u / d^(y) slices stay in L2
+  int defL = kBlockLDefault, defR = kBlockRDefault;
+  if (c->kind == K_MATCH) {
+    defL = 1;
+    while (defL < 31 && (int64_t(1) << defL) < c->nprime) ++defL;
+    defR = 22;
+  }
+  const int kBlockL = eL ? atoi(eL) : defL, kBlockR = eR ? atoi(eR) : defR;
   // packing rows in degree-descending order (fast path only; hooks restore vertex order)
   int32_t* prowf = talloc<int32_t>(c->nv);
   {

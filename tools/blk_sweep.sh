@@ -1,7 +1,7 @@
 # bench c4 under several L2-block shapes (MWU_BLOCK_L / MWU_BLOCK_R)
 set -u
 mkdir -p gpurun_out
-for lr in "22 20" "21 20" "23 21" "22 21" "21 19" "20 20"; do
+for lr in "22 20" "24 22" "24 21" "24 20" "24 19"; do
   set -- $lr
   echo "== $1 $2" >> gpurun_out/blk2.log
   MWU_BLOCK_L=$1 MWU_BLOCK_R=$2 timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu --no-e2e 2>&1 | python -c "
