@@ -1538,7 +1538,13 @@ struct Buckets {
   int shift, nb;
 };
 
-__global__ void __launch_bounds__(MWU_NT, 3) col_match_fast(int64_t E, const int32_t* __restrict__ srow,
+#ifndef MWU_MATCH_MINB
+#define MWU_MATCH_MINB 3
+#endif
+#ifndef MWU_MATCH_U
+#define MWU_MATCH_U 2         // edges per thread per grid-stride step
+#endif
+__global__ void __launch_bounds__(MWU_NT, MWU_MATCH_MINB) col_match_fast(int64_t E, const int32_t* __restrict__ srow,
                                                          const int32_t* __restrict__ drow,
                                                          const double* __restrict__ u, double* __restrict__ x,
                                                          double* __restrict__ d, double* __restrict__ dy,
@@ -1549,7 +1555,7 @@ __global__ void __launch_bounds__(MWU_NT, 3) col_match_fast(int64_t E, const int
   const int apply = c->apply_prev;
   const int lane = threadIdx.x & 31;
   double acc[2] = {-INFINITY, 0.0};
-  constexpr int U = 2;
+  constexpr int U = MWU_MATCH_U;
   const int64_t chunk = (int64_t)U * MWU_NT;
   for (int64_t base = (int64_t)blockIdx.x * chunk; base < E; base += (int64_t)gridDim.x * chunk) {
     double xe[U], dp[U], us[U], ud[U];

@@ -619,7 +619,7 @@ void build_blocked_order(mwu_ctx* c) {
   {
     unsigned long long *dk = talloc<unsigned long long>(c->nv), *dko = talloc<unsigned long long>(c->nv);
     uint32_t *dv = talloc<uint32_t>(c->nv), *dvo = talloc<uint32_t>(c->nv);
-    k_deg_keys<<<grid_for(c, c->nv), MWU_NT, 0, c->st>>>(c->nv, c->deg, dk, dv);
+    k_deg_keys<<<grid_for(c, c->nv), MWU_NT, 0, c->st>>>(c->nv, c->deg, c->kind == K_MATCH ? c->nleft : 0, dk, dv);
     CKL();
     size_t tb2 = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tb2, dk, dko, dv, dvo, c->nv, 0, 64, c->st));
@@ -785,8 +785,8 @@ void enqueue_column(mwu_ctx* c, cudaStream_t st) {
     case K_MATCH:
       if (c->scatterP) {
         CK(cudaMemsetAsync(c->dy, 0, (c->mP > 0 ? c->mP : 1) * sizeof(double), st));
-        const int64_t blocks = (c->E + 2 * MWU_NT - 1) / (2 * MWU_NT);
-        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, 3 * c->sms));
+        const int64_t blocks = (c->E + MWU_MATCH_U * MWU_NT - 1) / (MWU_MATCH_U * MWU_NT);
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, MWU_MATCH_MINB * c->sms));
         if (c->bk.row) CK(cudaMemsetAsync(c->bk.cnt, 0, c->bk.nb * sizeof(int32_t), st));
         col_match_fast<<<g, MWU_NT, 0, st>>>(c->E, c->srow, c->drow, c->u, c->x, c->d, c->dy,
                                             c->record ? c->gdbg : nullptr, c->record ? c->hdbg : nullptr,

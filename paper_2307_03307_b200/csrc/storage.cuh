@@ -121,9 +121,14 @@ __global__ void k_block_keys(int64_t E, const int32_t* src, const int32_t* dst, 
 
 // degree-descending row order (hot rows of power-law graphs cluster in a small, L2-resident
 // prefix of the packing-row vectors): key = (~deg, v)
-__global__ void k_deg_keys(int64_t nv, const int32_t* deg, unsigned long long* keys, uint32_t* vals) {
+// (bipartite: the left side's rows first, so a source sweep never touches right-side rows)
+__global__ void k_deg_keys(int64_t nv, const int32_t* deg, int64_t nleft, unsigned long long* keys, uint32_t* vals) {
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
-    keys[v] = ((unsigned long long)(0xffffffffu - (uint32_t)deg[v]) << 32) | (unsigned long long)v;
+    // isolated vertices last (rows [0, n') are the non-isolated ones), then side, then degree
+    const unsigned long long iso = deg[v] == 0 ? (1ull << 63) : 0ull;
+    const unsigned long long side = (nleft > 0 && v >= nleft) ? (1ull << 62) : 0ull;
+    keys[v] = iso | side | ((unsigned long long)(0x3fffffffu - ((uint32_t)deg[v] & 0x3fffffffu)) << 32) |
+              (unsigned long long)v;
     vals[v] = (uint32_t)v;
   }
 }
