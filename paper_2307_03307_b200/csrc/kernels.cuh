@@ -1328,6 +1328,9 @@ __device__ __forceinline__ bool act_bit(const uint32_t* act, int e) { return (__
 #ifndef MWU_COL_DENSE_XD
 #define MWU_COL_DENSE_XD 0    // 1: stage x and d of every edge too (measured slower: 2 stages only)
 #endif
+#ifndef MWU_SRC_DIRECT
+#define MWU_SRC_DIRECT 0      // 1: one reduction per active source slot instead of warp runs
+#endif
 #ifndef MWU_COL_MINB
 #define MWU_COL_MINB 2        // resident column CTAs per SM (grid = MWU_COL_MINB x SMs)
 #endif
@@ -1497,11 +1500,31 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
       if (d1 > 0.0) red_add_f64(dy + dr, invD * d1);              // dst side: random rows
 #endif
       // src side: edges are sorted by src, so lanes of a warp hold runs of equal rows
+#if MWU_SRC_DIRECT == 1
+      if (d0 > 0.0) red_add_f64(dy + sr, invD * d0);
+#elif MWU_SRC_DIRECT == 2
+      {
+        // warp runs only where a row repeats among the active lanes; else one reduction each
+        const double val = d0 > 0.0 ? invD * d0 : 0.0;
+        const int prev = __shfl_up_sync(0xffffffffu, sr, 1);
+        const bool dup = lane > 0 && prev == sr;
+        const uint32_t any = __ballot_sync(0xffffffffu, val > 0.0);
+        if (any) {
+          if (__any_sync(0xffffffffu, dup)) {
+            double run;
+            if (warp_run_sum(sr, val, run) && run > 0.0) red_add_f64(dy + sr, run);
+          } else if (val > 0.0) {
+            red_add_f64(dy + sr, val);
+          }
+        }
+      }
+#else
       const double val = d0 > 0.0 ? invD * d0 : 0.0;
       if (__any_sync(0xffffffffu, val > 0.0)) {
         double run;
         if (warp_run_sum(sr, val, run) && run > 0.0) red_add_f64(dy + sr, run);
       }
+#endif
     }
     // this warp is done with the stage: release it
     __syncwarp();
