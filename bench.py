@@ -260,7 +260,8 @@ def run_ours(args):
     # runs one replica per GPU
     sharded = (ws > 1 or args.shard) and args.workload in ("c2", "c3", "c4", "c5")
     make = Solver.graph_distributed if sharded else Solver.graph
-    S = make(kind, G.src, G.dst, G.n_vertices, G.n_left if kind == "bmatch" else 0, max_iter=args.max_iter)
+    opts = dict(max_iter=args.max_iter, block_l=args.block_l, block_r=args.block_r)
+    S = make(kind, G.src, G.dst, G.n_vertices, G.n_left if kind == "bmatch" else 0, **opts)
     st0 = S.stats()
     L, H, sense = bracket(kind, gs, eps)
 
@@ -354,7 +355,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
-        S2 = make(kind, src_h, dst_h, G.n_vertices, G.n_left if kind == "bmatch" else 0, max_iter=args.max_iter)
+        S2 = make(kind, src_h, dst_h, G.n_vertices, G.n_left if kind == "bmatch" else 0, **opts)
         S2.probe_begin(math.sqrt(L * H), eps)
         S = S2
         state.update({"L": L, "H": H, "B": math.sqrt(L * H)})
@@ -419,6 +420,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--solve", action="store_true", help="also time a full solve (time to (1+eps) solution)")
     ap.add_argument("--shard", action="store_true", help="sharded engine even with one rank (plumbing check)")
+    ap.add_argument("--block-l", type=int, default=0, help="mwu_options.block_l (0: default L2 block shape)")
+    ap.add_argument("--block-r", type=int, default=0, help="mwu_options.block_r (0: default L2 block shape)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -110,6 +110,21 @@ typedef struct {
                          /* (default): the forward product of graph kinds is scattered with fp64 */
                          /* atomics into the L2-resident vertex vector (summation order varies   */
                          /* run to run at the 1e-16 level)                          */
+  void *stream;          /* cudaStream_t on which the caller produces the input buffers and       */
+                         /* consumes the outputs (e.g. torch.cuda.current_stream()); NULL = the    */
+                         /* legacy default stream.  Every call that reads or writes caller memory */
+                         /* first makes the library's internal stream wait for work queued on it,  */
+                         /* and returns only once its outputs are complete (mwu_set_stream moves   */
+                         /* a context to another stream).                                          */
+  int block_l, block_r;  /* L2-blocked internal edge order of the fast edge-variable path         */
+                         /* (the paper's CSB tiles P:901-923 at L2 scale): source /  */
+                         /* destination row blocks of 2^block_l / 2^block_r packing rows; 0 =     */
+                         /* per-kind defaults (densest 22 / 20, matching one source block / 22).  */
+                         /* Result-neutral up to summation order; tests force small blocks so     */
+                         /* multi-block orders run under the parity checks.                        */
+  int compact_cover;     /* vcover / domset on one rank: the forward product compacts the covering */
+                         /* rows with d^(z) > 0 for the search passes (1, default); 0 streams all  */
+                         /* covering rows.  Result-neutral up to summation order.   */
 } mwu_options;
 
 typedef struct {
@@ -126,6 +141,17 @@ typedef struct {
   double t_create_ms, t_solve_ms, t_loop_ms;
   double bytes_alg_per_iter;         /* algorithmic HBM bytes of one MWU iteration   */
   int64_t kernel_launches;           /* kernels launched by the last solve / probe run            */
+  /* ---- SURVEY §8(b) additions */
+  int64_t near_tie_count;            /* decisions taken within 1e-12 relative of their threshold   */
+                                     /* (f(alpha) >= 1, min z >= 1, rho <= 1+eps; Q22), all probes */
+  double t_phase_ms[4];              /* device time by phase, all probes of the last solve / run:  */
+                                     /* [0] column (transposed products, direction; fused scatter  */
+                                     /* of d^(y) on the fast paths), [1] step (forward products),  */
+                                     /* [2] step search passes, [3] update (y, z, weights); from    */
+                                     /* %globaltimer at the end of each phase, gaps included        */
+  double max_Px_raw, min_Cx_raw;     /* max y and min z of the feasible probe's final iterate x    */
+  double max_Px, min_Cx;             /* the same for the returned x_out = x / min(Cx) (Q15):        */
+                                     /* max_Px = certificate, min_Cx = 1; NaN if none               */
 } mwu_stats;
 
 /* Vector ids for mwu_get_vec (per-iteration parity, BASELINE north_star): */
@@ -214,6 +240,9 @@ mwu_status mwu_run_iters(mwu_ctx *ctx, int64_t k, int32_t *state);
 mwu_status mwu_get_vec(mwu_ctx *ctx, int which, double *out, int64_t len);
 /* Length of vector `which` in the current probe (0 if unavailable). */
 int64_t mwu_vec_len(mwu_ctx *ctx, int which);
+
+/* Make the context order its caller-memory reads / writes after `stream` (see mwu_options). */
+mwu_status mwu_set_stream(mwu_ctx *ctx, void *stream);
 
 /* Record g and h in every iteration (parity tests); costs 16 bytes/variable/iteration. */
 mwu_status mwu_set_record(mwu_ctx *ctx, int on);

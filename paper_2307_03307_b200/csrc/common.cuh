@@ -109,7 +109,27 @@ struct Ctl {
   // ---- CUDA graph conditional handles (0 when host-driven)
   unsigned long long h_iter, h_search;
   int32_t nan_flag, pad_;
+  // ---- diagnostics: decisions within 1e-12 of their threshold (Q22) and device time by phase
+  // (column, step, search, update), from %globaltimer at the end of each phase (ns)
+  int64_t near_ties;
+  unsigned long long tmark;
+  double tph[4];
 };
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// close the phase that ends now: the time since the previous phase end goes to phase p
+__device__ __forceinline__ void phase_mark(Ctl* c, int p) {
+  const unsigned long long t = globaltimer_ns();
+  if (p >= 0 && c->tmark) c->tph[p] += (double)(t - c->tmark);
+  c->tmark = t;
+}
+__device__ __forceinline__ bool near_tie(double a, double b) {
+  return fabs(a - b) <= 1e-12 * fmax(fabs(a), fabs(b));
+}
 
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ double red_identity(int op) {

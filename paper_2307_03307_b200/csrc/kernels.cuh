@@ -16,9 +16,6 @@
 #pragma once
 #include "common.cuh"
 #include "fastmath.cuh"
-#ifndef MWU_ABLATE
-#define MWU_ABLATE 0
-#endif
 
 namespace mwu {
 
@@ -212,6 +209,7 @@ __device__ void search_controller(Ctl* c, const double* res) {
       if (nP || nC) { if (lse_j < 0) lse_j = j; continue; }
       const double mxj = cand_mx(c, j, res), mnj = cand_mn(c, j, res);
       const bool ok = phi >= psi;                                  // eq:b4b_conv
+      if (near_tie(phi, psi) || near_tie(mnj, 1.0)) c->near_ties++;
       if (ok && mnj < 1.0) { c->dk_lo = k; c->ok_mx = mxj; c->ok_mn = mnj; c->ok_tc = cand_tc(c, j, res); c->ok_sh = cand_sh(c, j); }
       else {
         c->dk_hi = k; c->hi_exit = ok ? 1 : 0; c->hi_mx = mxj; c->hi_mn = mnj;
@@ -287,6 +285,7 @@ __device__ void search_controller(Ctl* c, const double* res) {
       return;
     }
     const bool ok = phi >= psi;                                             // eq:b4b_conv
+    if (near_tie(phi, psi)) c->near_ties++;
     c->evals++;
     c->evals_total++;
     if (ok) { c->lb = need; c->lb_mx = mxj; c->lb_mn = mnj; c->lb_tc = cand_tc(c, j, res); c->lb_sh = cand_sh(c, j); }
@@ -299,6 +298,14 @@ __device__ void search_controller(Ctl* c, const double* res) {
 // Finalize: control logic run by thread 0 of the last block of a phase kernel
 // =====================================================================================
 __device__ void finalize(Ctl* c, int action, double* r) {
+  switch (action) {                        // phase timing: which phase ends with this action
+    case A_COL: case A_COL_FAST: phase_mark(c, 0); break;
+    case A_STEP_MAXDY: case A_STEP_DONE: case A_STEP_DONE + 100: case A_STEP_DONE_C: phase_mark(c, 1); break;
+    case A_SEARCH: phase_mark(c, 2); break;
+    case A_UPDATE: phase_mark(c, 3); break;
+    case A_INIT_W: phase_mark(c, -1); break;
+    default: break;
+  }
   switch (action) {
     case A_COL_FAST: {                             // fast densest column: max d, inactive aggregate
       c->apply_prev = 0;
@@ -365,6 +372,7 @@ __device__ void finalize(Ctl* c, int action, double* r) {
       if (c->t < 32) c->ahist[c->t] = c->alpha;
       c->t++;
       c->alpha_last = c->alpha; c->alpha_prev = c->alpha; c->apply_prev = 1;
+      if (near_tie(c->cSing ? c->zS + c->alpha * c->dzS : c->newsC, 1.0)) c->near_ties++;   // min z >= 1
       if (c->pSing) { c->yS = c->yS + c->alpha * c->dyS; c->sP = c->yS; c->SP = 1.0; }
       else { c->sP = c->newsP; c->SP = r[0]; }
       if (c->cSing) { c->zS = c->zS + c->alpha * c->dzS; c->sC = c->zS; c->SC = 1.0; }
@@ -1296,15 +1304,20 @@ __global__ void __launch_bounds__(MWU_NT) reduce_vec(int64_t n, const double* __
 // with fp64 reductions into the (L2-resident) vertex vector, and per-tile compaction of the
 // covering rows with d^(z) > 0 for the search passes.
 // =====================================================================================
-// Warp-segmented sum over lanes holding nondecreasing keys (edges sorted by src): the last lane
-// of each run of equal keys returns the run's sum in `out` (others return false).
+// Warp-segmented sum over runs of equal keys held by consecutive lanes (edges sorted by src row,
+// or any order: a key that reappears after a different key starts a new run).  The last lane
+// of each run returns the run's sum in `out` (others return false).  The scan adds lane - o only
+// when it lies inside the lane's own run (run start from a ballot of the heads), so keys
+// A, B, A in one warp are three runs, never one.
 __device__ __forceinline__ bool warp_run_sum(int key, double val, double& out) {
   const int lane = threadIdx.x & 31;
+  const int pk = __shfl_up_sync(0xffffffffu, key, 1);
+  const uint32_t heads = __ballot_sync(0xffffffffu, lane == 0 || pk != key);
+  const int start = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));   // first lane of my run
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const double ov = __shfl_up_sync(0xffffffffu, val, o);
-    const int ok = __shfl_up_sync(0xffffffffu, key, o);
-    if (lane >= o && ok == key) val += ov;
+    if (lane - o >= start) val += ov;
   }
   const int nk = __shfl_down_sync(0xffffffffu, key, 1);
   out = val;
@@ -1325,38 +1338,25 @@ __device__ __forceinline__ bool act_bit(const uint32_t* act, int e) { return (__
 // shared memory by the bulk-copy engine (cp.async.bulk + mbarrier) kColStages tiles ahead; the
 // u gathers of tile i+1 are issued (registers) before tile i is computed.  Stages are released per warp (an 8-arrival "empty" mbarrier), so
 // only the producer thread waits for the slowest warp; no block-wide barrier in the loop.
-#ifndef MWU_COL_DENSE_XD
-#define MWU_COL_DENSE_XD 0    // 1: stage x and d of every edge too (measured slower: 2 stages only)
-#endif
-#ifndef MWU_SRC_DIRECT
-#define MWU_SRC_DIRECT 0      // 1: one reduction per active source slot instead of warp runs
-#endif
 #ifndef MWU_COL_MINB
 #define MWU_COL_MINB 2        // resident column CTAs per SM (grid = MWU_COL_MINB x SMs)
 #endif
 #ifndef MWU_COL_STAGES
 #define MWU_COL_STAGES 4
 #endif
-constexpr int kColStages = MWU_COL_DENSE_XD ? 2 : MWU_COL_STAGES;
+constexpr int kColStages = MWU_COL_STAGES;
 constexpr int kColOffS = MWU_CT * 8, kColOffD = kColOffS + MWU_CT * 4, kColOffA = kColOffD + MWU_CT * 4;
-constexpr int kColOffX = ((kColOffA + (MWU_CT / 32) * 4) + 127) / 128 * 128;   // x pairs, then d pairs
-constexpr int kColOffDD = kColOffX + MWU_CT * 16;
-constexpr int kColStageBytes = MWU_COL_DENSE_XD ? kColOffDD + MWU_CT * 16 : kColOffX;
+constexpr int kColStageBytes = ((kColOffA + (MWU_CT / 32) * 4) + 127) / 128 * 128;
 constexpr size_t kColSmem = (size_t)kColStages * kColStageBytes;
 
 __device__ __forceinline__ uint32_t r16(uint32_t b) { return (b + 15u) & ~15u; }
 
 __device__ __forceinline__ void col_issue(char* stage, uint64_t* bar, int tile, int E, const double* z,
-                                          const int32_t* srow, const int32_t* drow, const uint32_t* act,
-                                          const double* x, const double* d) {
+                                          const int32_t* srow, const int32_t* drow, const uint32_t* act) {
   const int e0 = tile * MWU_CT;
   const int rows = min(MWU_CT, E - e0);
   const uint32_t bz = r16(rows * 8u), bi = r16(rows * 4u), ba = r16(((rows + 31) / 32) * 4u);
-  mbar_expect_tx(bar, bz + 2 * bi + ba + (MWU_COL_DENSE_XD ? 2 * rows * 16u : 0u));
-  if (MWU_COL_DENSE_XD) {
-    tma_load_1d(stage + kColOffX, x + 2 * (int64_t)e0, rows * 16u, bar);
-    tma_load_1d(stage + kColOffDD, d + 2 * (int64_t)e0, rows * 16u, bar);
-  }
+  mbar_expect_tx(bar, bz + 2 * bi + ba);
   const uint64_t pf = pol_first();
   tma_load_1d_hint(stage, z + e0, bz, bar, pf);
   tma_load_1d_hint(stage + kColOffS, srow + e0, bi, bar, pf);
@@ -1405,7 +1405,7 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
   __syncthreads();
   if (threadIdx.x == 0)
     for (int k = 0; k < mine && k < kColStages; ++k)
-      col_issue(csm + k * kColStageBytes, &full[k], blockIdx.x + k * gridDim.x, E, z, srow, drow, act, x, d);
+      col_issue(csm + k * kColStageBytes, &full[k], blockIdx.x + k * gridDim.x, E, z, srow, drow, act);
   double us[kColEdges], ud[kColEdges], nus[kColEdges], nud[kColEdges];
   if (mine > 0) {
     mbar_wait(&full[0], 0u);
@@ -1437,12 +1437,7 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
       const int j = k * MWU_NT + threadIdx.x;
       pw[k] = j < rows ? sac[j >> 5] : 0u;
       had[k] = (pw[k] >> lane) & 1u;
-      if (MWU_COL_DENSE_XD) {
-        if (j < rows) {
-          xe[k] = reinterpret_cast<const double2*>(stg + kColOffX)[j];
-          dp[k] = reinterpret_cast<const double2*>(stg + kColOffDD)[j];
-        }
-      } else if (had[k]) { xe[k] = x2[e0 + j]; dp[k] = d2[e0 + j]; }
+      if (had[k]) { xe[k] = x2[e0 + j]; dp[k] = d2[e0 + j]; }
     }
     // compaction of the active covering rows: each warp owns the record segment
     // [tile*CT + warp*kWarpSeg, +kWarpSeg) of its kWarpSeg edges, filled in (k, lane) order
@@ -1465,22 +1460,14 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
           zz = zz + ap * dzp;
           z[e] = zz;
         }
-#if MWU_ABLATE == 2
-        v = 1.0 + neta * (zz - sC);
-#else
         v = mwu_exp_tab(neta * (zz - sC), s_tab);                 // covering weight (Q4)
-#endif
         const double h = v * rSC;                                 // W^T w_c
-#if MWU_ABLATE == 1
-        const double g0 = invD * (zz * rSP), g1 = invD * (zz * 0.5 * rSP);
-#else
         const double g0 = invD * (us[k] * rSP);                   // (1/D) O^T w_p
         const double g1 = invD * (ud[k] * rSP);
-#endif
         if (gdbg) { gdbg[2 * e] = g0; gdbg[2 * e + 1] = g1; hdbg[2 * e] = h; hdbg[2 * e + 1] = h; }
         // g >= h gives fl(g/h) >= 1, i.e. d = 0 exactly
         const bool a0 = g0 < h, a1 = g1 < h;
-        if (!MWU_COL_DENSE_XD && (a0 || a1) && !had[k]) xe[k] = x2[e];   // newly active: fetch x
+        if ((a0 || a1) && !had[k]) xe[k] = x2[e];   // newly active: fetch x
         if (a0) d0 = mwu_direction(g0, h, xe[k].x, sigma);
         if (a1) d1 = mwu_direction(g1, h, xe[k].y, sigma);
       }
@@ -1496,35 +1483,13 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
       } else if (valid) { im = zz < im ? zz : im; is += v; }       // candidate-independent row
       wp += __popc(bw);
       if (lane == 0 && valid && bw != pw[k]) act[e >> 5] = bw;
-#if MWU_ABLATE != 3
       if (d1 > 0.0) red_add_f64(dy + dr, invD * d1);              // dst side: random rows
-#endif
-      // src side: edges are sorted by src, so lanes of a warp hold runs of equal rows
-#if MWU_SRC_DIRECT == 1
-      if (d0 > 0.0) red_add_f64(dy + sr, invD * d0);
-#elif MWU_SRC_DIRECT == 2
-      {
-        // warp runs only where a row repeats among the active lanes; else one reduction each
-        const double val = d0 > 0.0 ? invD * d0 : 0.0;
-        const int prev = __shfl_up_sync(0xffffffffu, sr, 1);
-        const bool dup = lane > 0 && prev == sr;
-        const uint32_t any = __ballot_sync(0xffffffffu, val > 0.0);
-        if (any) {
-          if (__any_sync(0xffffffffu, dup)) {
-            double run;
-            if (warp_run_sum(sr, val, run) && run > 0.0) red_add_f64(dy + sr, run);
-          } else if (val > 0.0) {
-            red_add_f64(dy + sr, val);
-          }
-        }
-      }
-#else
+      // src side: edges are sorted by src within an L2 block, so lanes hold runs of equal rows
       const double val = d0 > 0.0 ? invD * d0 : 0.0;
       if (__any_sync(0xffffffffu, val > 0.0)) {
         double run;
         if (warp_run_sum(sr, val, run) && run > 0.0) red_add_f64(dy + sr, run);
       }
-#endif
     }
     // this warp is done with the stage: release it
     __syncwarp();
@@ -1532,7 +1497,7 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
     if (lane == 0) tcnt[tile * (MWU_NT / 32) + warp] = wp - seg0;
     if (threadIdx.x == 0 && kt + kColStages < mine) {           // producer: refill once all warps left
       mbar_wait(&empty[slot], (uint32_t)((kt / kColStages) & 1));
-      col_issue(stg, &full[slot], blockIdx.x + (kt + kColStages) * gridDim.x, E, z, srow, drow, act, x, d);
+      col_issue(stg, &full[slot], blockIdx.x + (kt + kColStages) * gridDim.x, E, z, srow, drow, act);
     }
   };
   for (int kt = 0; kt < mine; ++kt) {
@@ -1549,18 +1514,6 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
 // g_e = w_p[r(src)] + w_p[r(dst)] (M^T), d_e, and the forward product
 // d^(y) = M d scattered into the vertex vector (src side: warp-segmented runs of the sorted edge
 // list; dst side: one fp64 reduction per nonzero d_e).  Reduces max d and sum(d)/M.
-// Propagation blocking of the random (dst) side of the scattered forward product when the
-// packing-row vector is far beyond L2 (c5): the column kernel appends (row, value) to the bucket
-// of the row's 1M-row range (warp-aggregated cursor atomics, L2-combined writes), then
-// bucket_flush adds each bucket into its L2-resident 8 MB slice of d^(y), bucket after bucket.
-struct Buckets {
-  int32_t* row;          // [capacity] (nullptr: scatter directly)
-  double* val;
-  const int64_t* base;   // [nb + 1] static capacities (dst-row histogram of the local edges)
-  int32_t* cnt;          // [nb] fill of this iteration
-  int shift, nb;
-};
-
 #ifndef MWU_MATCH_MINB
 #define MWU_MATCH_MINB 3
 #endif
@@ -1572,7 +1525,7 @@ __global__ void __launch_bounds__(MWU_NT, MWU_MATCH_MINB) col_match_fast(int64_t
                                                          const double* __restrict__ u, double* __restrict__ x,
                                                          double* __restrict__ d, double* __restrict__ dy,
                                                          double* gdbg, double* hdbg, Ctl* c, double* part,
-                                                         unsigned int* counter, Buckets bk) {
+                                                         unsigned int* counter) {
   if (c->status != ST_RUNNING) return;
   const double rSP = 1.0 / c->SP, invB = c->invB, sigma = c->sigma, ap = c->alpha_prev;
   const int apply = c->apply_prev;
@@ -1591,11 +1544,7 @@ __global__ void __launch_bounds__(MWU_NT, MWU_MATCH_MINB) col_match_fast(int64_t
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-#if MWU_ABLATE == 1
-      if (sr[k] >= 0) { us[k] = __ldg(u + sr[k]); ud[k] = us[k]; }
-#else
       if (sr[k] >= 0) { us[k] = __ldg(u + sr[k]); ud[k] = __ldg(u + dr[k]); }
-#endif
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
@@ -1611,29 +1560,7 @@ __global__ void __launch_bounds__(MWU_NT, MWU_MATCH_MINB) col_match_fast(int64_t
         acc[1] += invB * de;
       }
       const bool want = de > 0.0;
-      if (bk.row) {                                               // dst side, bucketed
-        // warp-aggregated cursor per distinct bucket (full-mask intrinsics in a uniform loop)
-        const int b = want ? (dr[k] >> bk.shift) : -1;
-        unsigned m = __ballot_sync(0xffffffffu, want);
-        while (m) {
-          const int leader = __ffs(m) - 1;
-          const int lb = __shfl_sync(0xffffffffu, b, leader);
-          const unsigned grp = __ballot_sync(0xffffffffu, want && b == lb);
-          int pos = 0;
-          if (lane == leader) pos = atomicAdd(bk.cnt + lb, __popc(grp));
-          pos = __shfl_sync(0xffffffffu, pos, leader);
-          if (want && b == lb) {
-            const int64_t slot = bk.base[lb] + pos + __popc(grp & ((1u << lane) - 1u));
-            bk.row[slot] = dr[k];
-            bk.val[slot] = de;
-          }
-          m &= ~grp;
-        }
-      } else {
-#if MWU_ABLATE != 3
-        if (want) red_add_f64(dy + dr[k], de);                    // dst side
-#endif
-      }
+      if (want) red_add_f64(dy + dr[k], de);                      // dst side
       if (__any_sync(0xffffffffu, want)) {                        // src side: sorted runs
         double run;
         if (warp_run_sum(sr[k], de, run) && run > 0.0) red_add_f64(dy + sr[k], run);
@@ -1642,25 +1569,6 @@ __global__ void __launch_bounds__(MWU_NT, MWU_MATCH_MINB) col_match_fast(int64_t
   }
   const int ops[2] = {OP_MAX, OP_SUM};
   reduce_and_finalize<2>(acc, ops, part, counter, c, A_COL);
-}
-
-// Second half of the propagation blocking: slots in bucket order (the grid's window stays in one
-// or two buckets, whose d^(y) slice is L2-resident); unfilled capacity is skipped.
-__global__ void __launch_bounds__(MWU_NT) bucket_flush(int64_t cap, const int32_t* __restrict__ brow,
-                                                       const double* __restrict__ bval, const int64_t* __restrict__ base,
-                                                       const int32_t* __restrict__ cnt, int nb, double* __restrict__ dy,
-                                                       const Ctl* c) {
-  if (c->status != ST_RUNNING) return;
-  extern __shared__ int64_t sb[];               // [nb + 1] bases, then [nb] fills
-  int64_t* sfill = sb + nb + 1;
-  for (int i = threadIdx.x; i <= nb; i += MWU_NT) sb[i] = base[i];
-  for (int i = threadIdx.x; i < nb; i += MWU_NT) sfill[i] = cnt[i];
-  __syncthreads();
-  for (int64_t s = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; s < cap; s += (int64_t)gridDim.x * MWU_NT) {
-    int lo = 0, hi = nb - 1;                    // bucket of slot s: last b with base[b] <= s
-    while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (sb[mid] <= s) lo = mid; else hi = mid - 1; }
-    if (s - sb[lo] < sfill[lo]) red_add_f64(dy + __ldcs(brow + s), __ldcs(bval + s));
-  }
 }
 
 // Init forward product y = P x of the edge-variable kinds by scatter (fast path):

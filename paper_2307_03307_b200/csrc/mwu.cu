@@ -81,8 +81,6 @@ struct mwu_ctx {
   int scatterP = 0;          // graph kinds with edge variables: d^(y) scattered by the column kernel
   uint32_t* perm = nullptr;  // scatterP: internal (L2-blocked) edge position -> original edge id
   uint32_t* rowperm = nullptr;  // scatterP: fast (degree-ordered) packing row -> vertex-order row
-  Buckets bk{};                 // bmatch with an out-of-L2 packing side: propagation blocking
-  int64_t bkcap = 0;
   int compC = 0;             // vcover (fast, one rank): forward product writes compacted covering records
   int fastC = 0;             // vcover / domset: transposed (and domset forward) products scattered
   double* exptab = nullptr;  // 2^(j/256), j < 256 (fastmath.cuh mwu_exp_tab)
@@ -126,6 +124,8 @@ struct mwu_ctx {
   int64_t launches = 0;
   double bytes_alg = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t evin = nullptr;   // caller-stream ordering (mwu_options.stream)
+  cudaStream_t ust = nullptr;   // the caller's stream (nullptr: legacy default stream)
 };
 
 namespace {
@@ -165,6 +165,13 @@ int bits_for(int64_t n) {
 }
 
 void sync(mwu_ctx* c) { CK(cudaStreamSynchronize(c->st)); }
+
+// Order the library stream after the work the caller queued on its stream (mwu_options.stream):
+// called before every read of caller memory; outputs are complete when a call returns.
+void wait_caller(mwu_ctx* c) {
+  CK(cudaEventRecord(c->evin, c->ust ? c->ust : cudaStreamLegacy));
+  CK(cudaStreamWaitEvent(c->st, c->evin, 0));
+}
 
 template <class T>
 T read_scalar(mwu_ctx* c, const T* dptr) {
@@ -352,6 +359,9 @@ void init_ctx_common(mwu_ctx* c, const mwu_options* opt) {
   CK(cudaMemsetAsync(c->counter, 0, sizeof(unsigned int), c->st));
   CK(cudaEventCreate(&c->ev0));
   CK(cudaEventCreate(&c->ev1));
+  CK(cudaEventCreateWithFlags(&c->evin, cudaEventDisableTiming));
+  c->ust = (cudaStream_t)c->opt.stream;
+  wait_caller(c);
 }
 
 // ------------------------------------------------------------------------------ graph build
@@ -594,17 +604,9 @@ const double* gather_full(mwu_ctx* c, const double* local, int w) {
 // endpoint rows of the internal order.  perm maps internal -> original edge ids (Q29 order is
 // restored by every vector hook and mwu_get_x).
 constexpr int kBlockLDefault = 22, kBlockRDefault = 20;   // src blocks of 4M rows, dst blocks of 1M rows
-// env knob: NAME=0 turns a default-on fast-path feature off (experiments / A-B runs)
-bool getenv_flag_off(const char* name) {
-  const char* e = getenv(name);
-  return e && atoi(e) == 0;
-}
-
 void build_blocked_order(mwu_ctx* c) {
   const int64_t E = c->E;
   if (E <= 0) return;
-  const char* eL = getenv("MWU_BLOCK_L");      // experiment knobs
-  const char* eR = getenv("MWU_BLOCK_R");
   // matching (random bipartite, degree ~16: no src-block reuse): one source block
   // (edges sorted by src row) and 4M-row destination blocks whose u / d^(y) slices stay in L2
   int defL = kBlockLDefault, defR = kBlockRDefault;
@@ -613,7 +615,9 @@ void build_blocked_order(mwu_ctx* c) {
     while (defL < 31 && (int64_t(1) << defL) < c->nprime) ++defL;
     defR = 22;
   }
-  const int kBlockL = eL ? atoi(eL) : defL, kBlockR = eR ? atoi(eR) : defR;
+  const int kBlockL = c->opt.block_l > 0 ? c->opt.block_l : defL;
+  const int kBlockR = c->opt.block_r > 0 ? c->opt.block_r : defR;
+  if (kBlockL > 31 || kBlockR > 31) throw MwuError{MWU_ERR_ARG, "block_l / block_r must be <= 31"};
   // packing rows in degree-descending order (fast path only; hooks restore vertex order)
   int32_t* prowf = talloc<int32_t>(c->nv);
   {
@@ -661,40 +665,6 @@ const double* unperm(mwu_ctx* c, const double* in, int w) {
   k_unperm<<<grid_for(c, c->Eg), MWU_NT, 0, c->st>>>(c->Eg, c->perm_full, in, c->tmp2, w);
   CKL();
   return c->tmp2;
-}
-
-// Propagation blocking for bmatch (MWU_PB=1): static per-bucket capacities from the dst-row
-// histogram of the local edges.
-void build_buckets(mwu_ctx* c) {
-  if (c->kind != K_MATCH || !c->scatterP || c->E <= 0) return;
-  const char* env = getenv("MWU_PB");
-  // off by default: with 128 buckets and degree-ordered rows the global bucket cursors are a
-  // contention point (c5 column 440 ms vs 65 ms direct); per-CTA slot chunks
-  // would be needed
-  const bool on = env ? atoi(env) != 0 : false;
-  if (!on) return;
-  const int shift = 20;
-  const int nb = (int)((c->mP + (1 << shift) - 1) >> shift);
-  unsigned long long* hist = talloc<unsigned long long>(nb + 1);
-  CK(cudaMemsetAsync(hist, 0, (nb + 1) * sizeof(unsigned long long), c->st));
-  k_bucket_hist<<<grid_for(c, c->E), MWU_NT, 0, c->st>>>(c->E, c->drow, shift, hist);
-  CKL();
-  std::vector<unsigned long long> h(nb);
-  CK(cudaMemcpyAsync(h.data(), hist, nb * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->st));
-  sync(c);                                   // the context stream is non-blocking
-  tfree(hist);
-  std::vector<int64_t> base(nb + 1, 0);
-  for (int b = 0; b < nb; ++b) base[b + 1] = base[b] + (int64_t)h[b];
-  c->bkcap = base[nb];
-  int64_t* dbase = dalloc<int64_t>(c, nb + 1);
-  CK(cudaMemcpyAsync(dbase, base.data(), (nb + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->st));
-  sync(c);
-  c->bk.row = dalloc<int32_t>(c, c->bkcap);
-  c->bk.val = dalloc<double>(c, c->bkcap);
-  c->bk.base = dbase;
-  c->bk.cnt = dalloc<int32_t>(c, nb);
-  c->bk.shift = shift;
-  c->bk.nb = nb;
 }
 
 // ------------------------------------------------------------------------------ CSR build
@@ -787,18 +757,10 @@ void enqueue_column(mwu_ctx* c, cudaStream_t st) {
         CK(cudaMemsetAsync(c->dy, 0, (c->mP > 0 ? c->mP : 1) * sizeof(double), st));
         const int64_t blocks = (c->E + MWU_MATCH_U * MWU_NT - 1) / (MWU_MATCH_U * MWU_NT);
         const int g = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, MWU_MATCH_MINB * c->sms));
-        if (c->bk.row) CK(cudaMemsetAsync(c->bk.cnt, 0, c->bk.nb * sizeof(int32_t), st));
         col_match_fast<<<g, MWU_NT, 0, st>>>(c->E, c->srow, c->drow, c->u, c->x, c->d, c->dy,
                                             c->record ? c->gdbg : nullptr, c->record ? c->hdbg : nullptr,
-                                            c->ctl, c->part, c->counter, c->bk);
+                                            c->ctl, c->part, c->counter);
         c->launches++;
-        if (c->bk.row) {
-          const int gf = (int)std::max<int64_t>(1, std::min<int64_t>(4 * c->sms, (c->bkcap + MWU_NT - 1) / MWU_NT));
-          bucket_flush<<<gf, MWU_NT, (2 * c->bk.nb + 1) * sizeof(int64_t), st>>>(c->bkcap, c->bk.row, c->bk.val,
-                                                                              c->bk.base, c->bk.cnt, c->bk.nb,
-                                                                              c->dy, c->ctl);
-          c->launches++;
-        }
         break;
       }
       col_match<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, c->srow, c->drow, c->u, c->x, c->d,
@@ -1289,6 +1251,10 @@ void solve(mwu_ctx* c, double eps, int64_t max_iter, int32_t* outcome) {
   mwu_stats& S = c->stats;
   const int64_t l0 = c->launches;
   S.probes = 0; S.iters_total = 0; S.search_evals = 0; S.search_passes = 0;
+  S.near_tie_count = 0;
+  for (int p = 0; p < 4; ++p) S.t_phase_ms[p] = 0.0;
+  const double qnan = std::numeric_limits<double>::quiet_NaN();
+  S.max_Px_raw = S.min_Cx_raw = S.max_Px = S.min_Cx = qnan;
   S.certificate = std::numeric_limits<double>::quiet_NaN();
   S.objective = std::numeric_limits<double>::quiet_NaN();
   CK(cudaEventRecord(c->ev0, c->st));
@@ -1310,9 +1276,14 @@ void solve(mwu_ctx* c, double eps, int64_t max_iter, int32_t* outcome) {
     S.iters_last = h.t;
     S.search_evals += h.evals_total;
     S.search_passes += h.passes_total;
+    S.near_tie_count += h.near_ties;
+    for (int p = 0; p < 4; ++p) S.t_phase_ms[p] += h.tph[p] * 1e-6;
     S.outcome = h.status; S.reason = h.reason; S.eta = h.eta; S.alpha_last = h.alpha_last;
     if (h.status == ST_FEASIBLE) {
       S.certificate = h.sP / h.sC;      // rho = max y / min z (Q6)
+      if (std::fabs(S.certificate - (1.0 + eps)) <= 1e-12 * (1.0 + eps)) S.near_tie_count++;
+      S.max_Px_raw = h.sP; S.min_Cx_raw = h.sC;     // of the probe's final iterate
+      S.max_Px = S.certificate; S.min_Cx = 1.0;    // of x_out = x / min(Cx) (Q15)
       finish_feasible(c);
     }
     return h.status;
@@ -1328,15 +1299,17 @@ void solve(mwu_ctx* c, double eps, int64_t max_iter, int32_t* outcome) {
     const double rt = c->opt.outer_rel_tol > 0 ? c->opt.outer_rel_tol : eps / 4.0;
     const int sense = (c->mode == MWU_PURE_PACKING) ? +1 : -1;
     bool any = false;
-    double cert = std::numeric_limits<double>::quiet_NaN();
+    double cert = std::numeric_limits<double>::quiet_NaN(), raw[2] = {qnan, qnan};
     while (H > (1.0 + rt) * L) {
       const double B = std::sqrt(L * H);
       const int st = run_one(B);
       const bool ok = (st == ST_FEASIBLE);
-      if (ok) { any = true; cert = S.certificate; }
+      if (ok) { any = true; cert = S.certificate; raw[0] = S.max_Px_raw; raw[1] = S.min_Cx_raw; }
       if ((ok && sense > 0) || (!ok && sense < 0)) L = B; else H = B;
     }
     S.certificate = any ? cert : std::numeric_limits<double>::quiet_NaN();
+    S.max_Px_raw = raw[0]; S.min_Cx_raw = raw[1];
+    S.max_Px = S.certificate; S.min_Cx = any ? 1.0 : qnan;
     S.bound = sense > 0 ? L : H;
     if (c->kind == K_DENSEST) S.objective = S.bound;
     else { double s, mx; reduce_dev(c, c->xbest, c->n, s, mx); S.objective = s; }
@@ -1395,6 +1368,7 @@ void destroy_ctx(mwu_ctx* c) {
   if (c->hctl) cudaFreeHost(c->hctl);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->evin) cudaEventDestroy(c->evin);
   if (c->st) cudaStreamDestroy(c->st);
   delete c;
 }
@@ -1420,6 +1394,10 @@ void mwu_default_options(mwu_options* o) {
   o->nccl_id = nullptr;
   o->comm_group = nullptr;
   o->deterministic = 0;
+  o->stream = nullptr;
+  o->block_l = 0;
+  o->block_r = 0;
+  o->compact_cover = 1;
 }
 
 const char* mwu_last_error(const mwu_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
@@ -1477,9 +1455,8 @@ mwu_status mwu_create_graph(const mwu_graph* g, const mwu_options* opt, mwu_ctx*
     // vcover / domset, one rank: the forward product compacts the covering rows with d^(z) > 0
     // for the search passes (sharded runs keep the dense rows: their step reductions are not exchanged)
     c->compC = ((c->kind == K_VCOVER || c->kind == K_DOMSET) && c->fastC && !c->sharded && c->mC > 0 &&
-                c->mC < (int64_t(1) << 31) - MWU_CT && !getenv_flag_off("MWU_COMPC")) ? 1 : 0;
+                c->mC < (int64_t(1) << 31) - MWU_CT && c->opt.compact_cover) ? 1 : 0;
     alloc_vectors(c);
-    build_buckets(c);
     {                                        // exchange flags for reductions before a probe
       Ctl& h = *c->hctl;
       memset(&h, 0, sizeof(Ctl));
@@ -1603,6 +1580,7 @@ mwu_status mwu_get_x(mwu_ctx* c, double* x, int64_t len) {
   const int64_t n = c->ng > 0 ? c->ng : c->n;
   if (!x || len != n) { c->err = "mwu_get_x: len must equal n"; return MWU_ERR_ARG; }
   try {
+    wait_caller(c);
     const double* src = unperm(c, c->xbest, c->kind == K_DENSEST ? 2 : 1);
     CK(cudaMemcpyAsync(x, src, n * sizeof(double), cudaMemcpyDefault, c->st));
     sync(c);
@@ -1648,6 +1626,9 @@ mwu_status mwu_run_iters(mwu_ctx* c, int64_t k, int32_t* state) {
     c->stats.t_loop_ms = run_loop(c, k);
     pull_ctl(c);
     if (state) *state = c->hctl->status;
+    // probe-cumulative diagnostics of the current probe
+    c->stats.near_tie_count = c->hctl->near_ties;
+    for (int p = 0; p < 4; ++p) c->stats.t_phase_ms[p] = c->hctl->tph[p] * 1e-6;
     c->stats.kernel_launches = c->launches - l0;
   } catch (const MwuError& e) { return fail(c, e); }
   return MWU_OK;
@@ -1672,6 +1653,7 @@ mwu_status mwu_get_vec(mwu_ctx* c, int which, double* out, int64_t len) {
   const int64_t L = mwu_vec_len(c, which);
   if (!out || L <= 0 || len != L) { c->err = "mwu_get_vec: unknown vector or wrong length"; return MWU_ERR_ARG; }
   try {
+    wait_caller(c);
     pull_ctl(c);
     const Ctl h = *c->hctl;
     const double* src = nullptr;
@@ -1741,6 +1723,13 @@ mwu_status mwu_get_vec(mwu_ctx* c, int which, double* out, int64_t len) {
   return MWU_OK;
 }
 
+mwu_status mwu_set_stream(mwu_ctx* c, void* stream) {
+  GUARD(c);
+  c->ust = (cudaStream_t)stream;
+  c->opt.stream = stream;
+  return MWU_OK;
+}
+
 mwu_status mwu_set_record(mwu_ctx* c, int on) {
   GUARD(c);
   try {
@@ -1781,6 +1770,7 @@ mwu_status mwu_get_structure(mwu_ctx* c, int which, void* out, int64_t* bytes) {
   }
   if (*bytes < nb || !out) { *bytes = nb; c->err = "mwu_get_structure: buffer too small"; return MWU_ERR_ARG; }
   try {
+    wait_caller(c);
     CK(cudaMemcpyAsync(out, src, nb, cudaMemcpyDefault, c->st));
     sync(c);
   } catch (const MwuError& e) { return fail(c, e); }

@@ -142,11 +142,6 @@ __global__ void k_deg_rows(int64_t nprime, const uint32_t* vsorted, const int32_
   }
 }
 
-__global__ void k_bucket_hist(int64_t E, const int32_t* drow, int shift, unsigned long long* hist) {
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(hist + (drow[e] >> shift), 1ull);
-}
-
 __global__ void k_map_endpoints_perm(int64_t E, const uint32_t* perm, const int32_t* src, const int32_t* dst,
                                      const int32_t* prow, int32_t* srow, int32_t* drow) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x) {

@@ -11,7 +11,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.environ.get("MWU_SO") or os.path.join(_HERE, "libmwu.so")   # MWU_SO: ablation builds
+_SO = os.path.join(_HERE, "libmwu.so")
 
 OK, ERR_ARG, ERR_CUDA, ERR_OOM, ERR_NCCL, ERR_STATE, ERR_NUMERIC = range(7)
 RUNNING, FEASIBLE, INFEASIBLE, ITER_LIMIT = range(4)
@@ -45,7 +45,8 @@ class Options(ctypes.Structure):
                 ("max_evals", ctypes.c_int), ("outer_rel_tol", ctypes.c_double), ("use_graph", ctypes.c_int),
                 ("bisect_depth", ctypes.c_int), ("device", ctypes.c_int), ("world", ctypes.c_int),
                 ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p), ("comm_group", ctypes.c_void_p),
-                ("deterministic", ctypes.c_int)]
+                ("deterministic", ctypes.c_int), ("stream", ctypes.c_void_p), ("block_l", ctypes.c_int),
+                ("block_r", ctypes.c_int), ("compact_cover", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -56,14 +57,17 @@ class Stats(ctypes.Structure):
                 ("n", ctypes.c_int64), ("m_P", ctypes.c_int64), ("m_C", ctypes.c_int64), ("nnz_P", ctypes.c_int64),
                 ("nnz_C", ctypes.c_int64), ("empty_rows_dropped", ctypes.c_int64), ("t_create_ms", ctypes.c_double),
                 ("t_solve_ms", ctypes.c_double), ("t_loop_ms", ctypes.c_double),
-                ("bytes_alg_per_iter", ctypes.c_double), ("kernel_launches", ctypes.c_int64)]
+                ("bytes_alg_per_iter", ctypes.c_double), ("kernel_launches", ctypes.c_int64),
+                ("near_tie_count", ctypes.c_int64), ("t_phase_ms", ctypes.c_double * 4),
+                ("max_Px_raw", ctypes.c_double), ("min_Cx_raw", ctypes.c_double), ("max_Px", ctypes.c_double),
+                ("min_Cx", ctypes.c_double)]
 
 
 EXPORTS = ["mwu_default_options", "mwu_create_csr", "mwu_create_graph", "mwu_solve", "mwu_get_x",
            "mwu_get_stats", "mwu_destroy", "mwu_last_error", "mwu_probe_begin", "mwu_step", "mwu_run_probe",
            "mwu_run_iters", "mwu_get_vec", "mwu_vec_len", "mwu_set_record", "mwu_get_structure",
            "mwu_get_scalars", "mwu_get_unique_id", "mwu_profile_iters", "mwu_shard_range",
-           "mwu_simgroup_create", "mwu_simgroup_destroy"]
+           "mwu_simgroup_create", "mwu_simgroup_destroy", "mwu_set_stream"]
 
 _lib = None
 
@@ -97,6 +101,7 @@ def lib():
         L.mwu_vec_len.argtypes = [vp, ctypes.c_int]
         L.mwu_vec_len.restype = i64
         L.mwu_set_record.argtypes = [vp, ctypes.c_int]
+        L.mwu_set_stream.argtypes = [vp, vp]
         L.mwu_get_structure.argtypes = [vp, ctypes.c_int, vp, ctypes.POINTER(i64)]
         L.mwu_get_scalars.argtypes = [vp, ctypes.POINTER(dbl)]
         L.mwu_get_unique_id.argtypes = [vp]
@@ -111,9 +116,18 @@ def lib():
     return _lib
 
 
+def _current_stream():
+    """cudaStream_t of torch's current stream (None without CUDA): the caller-side ordering of
+    every ABI call that reads or writes tensors (mwu_options.stream)."""
+    if torch.cuda.is_available() and torch.cuda.is_initialized():
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return None
+
+
 def default_options(keep=None, **kw) -> Options:
     o = Options()
     lib().mwu_default_options(ctypes.byref(o))
+    o.stream = _current_stream()
     for k, v in kw.items():
         if not hasattr(o, k):
             raise TypeError(f"unknown option {k}")
@@ -234,7 +248,12 @@ class Solver:
         _check(lib().mwu_solve(self._h, float(eps), int(max_iter), ctypes.byref(out)), self._h)
         return OUTCOME_NAMES[out.value]
 
+    def _sync_stream(self):
+        st = _current_stream()
+        _check(lib().mwu_set_stream(self._h, st), self._h)
+
     def x(self, device="cuda") -> torch.Tensor:
+        self._sync_stream()
         t = torch.empty(self.n, dtype=torch.float64, device=device)
         _check(lib().mwu_get_x(self._h, _ptr(t), t.numel()), self._h)
         return t
@@ -243,6 +262,7 @@ class Solver:
         s = Stats()
         _check(lib().mwu_get_stats(self._h, ctypes.byref(s)), self._h)
         d = {k: getattr(s, k) for k, _ in Stats._fields_}
+        d["t_phase_ms"] = dict(zip(("column", "step", "search", "update"), list(s.t_phase_ms)))
         d["outcome"] = OUTCOME_NAMES.get(d["outcome"], str(d["outcome"]))
         d["reason"] = REASON_NAMES.get(d["reason"], str(d["reason"]))
         return d
@@ -274,6 +294,7 @@ class Solver:
         L = int(lib().mwu_vec_len(self._h, w))
         if L <= 0:
             raise MwuError(f"vector {which} unavailable")
+        self._sync_stream()
         t = torch.empty(L, dtype=torch.float64, device=device)
         _check(lib().mwu_get_vec(self._h, w, _ptr(t), L), self._h)
         return t

@@ -366,32 +366,53 @@ def test_host_buffers_e2e(cuda_ok):
     assert xh.device.type == "cpu"
 
 
-@pytest.mark.parametrize("kind,i", [("bmatch", 2), ("match", 1)])
-def test_bucketed_scatter_parity(cuda_ok, kind, i, monkeypatch):
-    """Propagation-blocked forward product (MWU_PB=1; off by default): the same
-    lockstep checks as the direct scatter."""
-    monkeypatch.setenv("MWU_PB", "1")
+@pytest.mark.parametrize("kind,i,bl,br", [("densest", 0, 6, 5), ("densest", 1, 7, 4), ("bmatch", 2, 5, 6),
+                                          ("match", 0, 6, 6), ("match", 1, 8, 5)])
+def test_small_block_order_parity(cuda_ok, kind, i, bl, br):
+    """The L2-blocked internal edge order with forced small row blocks, so that
+    edges cross many (source, destination) block pairs and a warp's 32 edges straddle block
+    boundaries (the source-side warp runs restart inside a warp): the same lockstep checks."""
     G = _graph(kind, i)
     s, d = G.numpy()
     B, _ = _oracle_probe_bound(kind, G)
     lp = O.graph_lp(kind, s, d, G.n_vertices, B)
     probe = O.Probe(lp, EPS[kind], max_iter=5000)
+    S = solver_for(kind, G, block_l=bl, block_r=br)
+    lockstep(S, probe, B, EPS[kind], 50, alphas=[1.0] * 50, strict_derived=True)
+
+
+@pytest.mark.parametrize("kind", ["vcover", "match", "densest"])
+def test_shuffled_edge_order_parity(cuda_ok, kind):
+    """Edge lists in random order (no generator sorting): the warp-segmented source-side sums
+    must treat a key that reappears after a different key as a new run (keys A, B, A in one
+    warp), in vcover's scatter over the caller's order and in the blocked kinds."""
+    G0 = {"vcover": gg.erdos_renyi(2000, 16000, seed=5), "match": gg.rmat(10, 8, seed=4),
+          "densest": gg.rmat(10, 16, seed=7)}[kind]
+    g = torch.Generator().manual_seed(123)
+    perm = torch.randperm(G0.n_edges, generator=g)
+    flip = torch.rand(G0.n_edges, generator=g) < 0.5
+    src, dst = G0.src[perm], G0.dst[perm]
+    src, dst = torch.where(flip, dst, src), torch.where(flip, src, dst)
+    G = gg.Graph(src.contiguous(), dst.contiguous(), G0.n_vertices)
+    s, d = G.numpy()
+    B, _ = _oracle_probe_bound(kind, G)
+    lp = O.graph_lp(kind, s, d, G.n_vertices, B)
+    probe = O.Probe(lp, EPS[kind], max_iter=5000)
     S = solver_for(kind, G)
-    lockstep(S, probe, B, EPS[kind], 50, alphas=None, window=self_sensitivity_window(lp, EPS[kind], None, 50))
+    lockstep(S, probe, B, EPS[kind], 50, alphas=[1.0] * 50, strict_derived=True)
 
 
 @pytest.mark.parametrize("kind", ["vcover", "domset"])
-@pytest.mark.parametrize("compc", ["0", "1"])
-def test_compact_covering_rows_parity(cuda_ok, kind, compc, monkeypatch):
+@pytest.mark.parametrize("compc", [0, 1])
+def test_compact_covering_rows_parity(cuda_ok, kind, compc):
     """The search over compacted covering records plus the inactive aggregate (default for
-    vcover / domset on one rank) and over the dense rows (MWU_COMPC=0): both under
-    the lockstep checks against the oracle, on both graphs of the kind."""
-    monkeypatch.setenv("MWU_COMPC", compc)
+    vcover / domset on one rank) and over the dense rows (compact_cover = 0): both
+    under the lockstep checks against the oracle, on both graphs of the kind."""
     for i in (0, 1):
         G = _graph(kind, i)
         s, d = G.numpy()
         B, _ = _oracle_probe_bound(kind, G)
         lp = O.graph_lp(kind, s, d, G.n_vertices, B)
         probe = O.Probe(lp, EPS[kind], max_iter=5000)
-        S = solver_for(kind, G)
+        S = solver_for(kind, G, compact_cover=compc)
         lockstep(S, probe, B, EPS[kind], 50, alphas=None, window=self_sensitivity_window(lp, EPS[kind], None, 50))
