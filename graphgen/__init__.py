@@ -9,5 +9,5 @@ from .generators import (  # noqa: F401
     Graph, CsrLP, bipartite_uniform, erdos_renyi, rmat, bipartite_zipf,
     complete_graph, complete_bipartite, star_graph, path_graph, cycle_graph,
     circulant_regular, random_small_graph, hub_graph, random_small_bipartite,
-    random_planted_lp, infeasible_lp, config_graph, CONFIGS,
+    random_planted_lp, infeasible_lp, config_graph, CONFIGS, disjoint_union, plus_random_edges,
 )

@@ -267,6 +267,36 @@ def hub_graph(n: int, hubs: int, hub_deg: int, extra: int, seed: int = 1) -> Gra
     return _finish(k // n, k % n, n, 0, f"hub({n},{hubs},{hub_deg},{extra})")
 
 
+def disjoint_union(*graphs: Graph) -> Graph:
+    """Vertex-disjoint union, edges in the order of the parts (ids shifted per part)."""
+    src, dst, off = [], [], 0
+    for g in graphs:
+        src.append(g.src.to(torch.int64) + off)
+        dst.append(g.dst.to(torch.int64) + off)
+        off += g.n_vertices
+    return _finish(torch.cat(src), torch.cat(dst), off, 0, "U(" + ";".join(g.name for g in graphs) + ")")
+
+
+def plus_random_edges(g: Graph, k: int, seed: int) -> Graph:
+    """g plus k extra distinct random edges (numpy PCG64 `default_rng(seed)`, appended in draw
+    order, endpoints as drawn) — a perturbed copy of a structured graph."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    s, d = g.numpy()
+    have = set(zip(s.tolist(), d.tolist())) | set(zip(d.tolist(), s.tolist()))
+    S, D = list(s), list(d)
+    while k:
+        a, b = rng.integers(0, g.n_vertices, 2)
+        if a != b and (a, b) not in have:
+            have.add((a, b))
+            have.add((b, a))
+            S.append(a)
+            D.append(b)
+            k -= 1
+    return Graph(torch.tensor(S, dtype=torch.int32), torch.tensor(D, dtype=torch.int32), g.n_vertices, 0,
+                 f"{g.name}+{len(S) - len(s)}r{seed}")
+
+
 # ---------------------------------------------------------- general CSR LPs
 def _random_csr(rows: int, n: int, density: float, g, lo=0.5, hi=2.0, min_per_row=1):
     mask = torch.rand(rows, n, generator=g, dtype=torch.float64) < density

@@ -149,33 +149,77 @@ def trajectory_errors(probe: O.Probe, st, ph, eta):
     return r
 
 
-def self_sensitivity_window(lp: O.LP, eps, alphas, iters, level=1e-12):
-    """Number of leading iterations over which the ORACLE, rerun from x0 perturbed by one ulp,
-    stays within `level` relative of itself (x, y, z): the window where any two correct fp64
-    evaluations of the searched MWU trajectory can agree to 1e-10 (conditioning)."""
-    a = O.Probe(lp, eps)
-    b = O.Probe(lp, eps)
-    b.x = b.x * (1 + 2.0 ** -52)
-    b.y, b.z = b.lp.P @ b.x, b.lp.C @ b.x
-    b._weights()
+DRIFT_KEYS = ("x", "y", "z", "wp", "wc", "g", "h", "d", "dy", "dz")
+DRIFT_FACTOR = 10.0   # GPU vs oracle allowed: max(1e-10, DRIFT_FACTOR x the oracle's own drift(t))
+
+
+def _probe_vecs(p: O.Probe):
+    v = dict(x=p.x, y=p.y, z=p.z, wp=p.u / p.SP, wc=p.v / p.SC)
+    for k in ("g", "h", "d", "dy", "dz"):
+        if k in p.last:
+            v[k] = p.last[k]
+    return v
+
+
+def self_drift(lp: O.LP, eps, alphas, iters, tol_mode="prose"):
+    """The ORACLE's own fp64 conditioning along the compared trajectory: it is rerun from x0
+    scaled by 1 +- 2^-52 (one ulp) with the same step rule, and drift[t][k] is the largest
+    elementwise relative difference (floor 1e-300) of vector k between the reruns and the
+    reference run after iteration t (t = 0: the initial state).  drift[t]["split"] is True once
+    a rerun accepted a different step size or terminated differently — a decision within the
+    rounding noise of Alg. 3 or of min z >= 1 (Q6), after which the trajectories
+    separate by the method itself.  Returns the list (length <= iters + 1)."""
+    runs = [O.Probe(lp, eps, tol_mode=tol_mode)] + [O.Probe(lp, eps, tol_mode=tol_mode, x0_scale=sc)
+                                                    for sc in (1 + 2.0 ** -52, 1 - 2.0 ** -52)]
+
+    def rec(split):
+        ref = _probe_vecs(runs[0])
+        r = {"split": split}
+        for k in DRIFT_KEYS:
+            if k in ref:
+                r[k] = max(rel_err(_probe_vecs(q)[k], ref[k]) for q in runs[1:])
+        return r
+    out = [rec(False)]
+    gone = {"split": True, **{k: float("inf") for k in DRIFT_KEYS}}
     for t in range(iters):
         al = None if alphas is None else alphas[t]
-        if a.step(al) != O.RUNNING or b.step(al) != O.RUNNING:
-            return t
-        if a.last["alpha"] != b.last["alpha"]:
-            return t
-        e = max(rel_err(b.x, a.x), rel_err(b.y, a.y), rel_err(b.z, a.z))
-        if e > level:
-            return t
-    return iters
+        sts = [q.step(al) for q in runs]
+        if any(q.status != runs[0].status for q in runs[1:]) or \
+                any(q.last.get("alpha") != runs[0].last.get("alpha") for q in runs[1:]):
+            out.append(gone)                   # a decision inside the rounding noise
+            break
+        if sts[0] != O.RUNNING:                # all terminated alike: nothing more to compare
+            break
+        out.append(rec(False))
+    return out
 
 
-def lockstep(solver, probe: O.Probe, bound, eps, iters, alphas=None, phase_check=True, window=None,
-             strict_derived=False):
+def drift_tol(drift, t, k, factor=DRIFT_FACTOR):
+    """Allowed GPU-vs-oracle relative error of vector k after iteration t."""
+    if t >= len(drift):
+        return float("inf")
+    return max(RTOL, factor * drift[t].get(k, 0.0))
+
+
+def self_sensitivity_window(lp: O.LP, eps, alphas, iters, level=1e-12):
+    """Number of leading iterations over which the ORACLE, rerun from x0 perturbed by one ulp,
+    stays within `level` relative of itself (x, y, z) — reported as a diagnostic."""
+    dr = self_drift(lp, eps, alphas, iters)
+    for t, r in enumerate(dr):
+        if r["split"] or max(r["x"], r["y"], r["z"]) > level:
+            return max(0, t - 1)
+    return len(dr) - 1
+
+
+def lockstep(solver, probe: O.Probe, bound, eps, iters, alphas=None, phase_check=True, drift=None,
+             strict_derived=False, factor=DRIFT_FACTOR):
     """Run `iters` MWU iterations on both sides (fixed steps `alphas`, or the Alg. 3 search on
-    both when None).  Asserts (A) every iteration; asserts (B) — state vectors within 1e-10,
-    weights within the propagated bound, identical alphas — for the first `window` iterations
-    (all of them when None); returns the per-iteration (B) error records."""
+    both when None).  Asserts (A) every iteration; asserts (B) — every compared vector within
+    max(1e-10, factor x the oracle's own one-ulp drift(t)) relative, identical step sizes — for
+    ALL iterations, with drift = self_drift(...) (None: the plain 1e-10 bound everywhere).
+    After the oracle's own reruns split (a decision inside the rounding noise) the trajectories
+    legitimately separate: (B) stops there, (A) continues from the GPU's own states.  Returns
+    the per-iteration (B) error records (with the bound used)."""
     solver.set_record(True)
     solver.probe_begin(bound, eps)
     sc = solver.scalars()
@@ -185,43 +229,46 @@ def lockstep(solver, probe: O.Probe, bound, eps, iters, alphas=None, phase_check
     recs = [trajectory_errors(probe, st, None, probe.eta)]
     for k in ("x", "y", "z"):
         assert recs[0][k] <= RTOL, (k, recs[0])
+    coupled = True                               # oracle trajectory still comparable under (B)
     for t in range(iters):
         a = None if alphas is None else alphas[t]
-        st_o = probe.step(alpha=a)
+        split = drift is not None and t + 1 < len(drift) and drift[t + 1]["split"]
+        st_o = probe.step(alpha=a) if coupled else O.RUNNING
         st_g = solver.step(0.0 if a is None else a)
-        if st_o == O.RUNNING and st_g in (O.FEASIBLE, O.ITER_LIMIT):
+        if coupled and st_o == O.RUNNING and st_g in (O.FEASIBLE, O.ITER_LIMIT):
             # the GPU tests termination right after the update; the oracle at the top of its next
             # step — one more oracle call must terminate without iterating
             t0 = probe.t
             st_o = probe.step(alpha=None if a is None else a)
-            assert probe.t == t0, "oracle iterated where the GPU terminated"
-            ph = gpu.phase()
-            new = gpu.state()
-            if phase_check:
-                phase_parity(probe.lp, probe.eta, probe.sigma, eps, st, ph, new, a)
-        if st_o != st_g:
+            assert probe.t == t0 or split, "oracle iterated where the GPU terminated"
+        if coupled and st_o != st_g and not split:
             raise AssertionError(f"iteration {t}: oracle {st_o}/{probe.reason} vs gpu {st_g}")
-        if st_o != O.RUNNING:
-            break
-        ph = gpu.phase()
+        ph = gpu.phase() if st_g == O.RUNNING or st_g in (O.FEASIBLE, O.ITER_LIMIT) else None
         new = gpu.state()
-        if phase_check:
+        if phase_check and ph is not None and st_g != O.INFEASIBLE:
             phase_parity(probe.lp, probe.eta, probe.sigma, eps, st, ph, new, a)
+        if st_g != O.RUNNING or (coupled and st_o != O.RUNNING and not split):
+            break
+        if coupled and split:
+            coupled = False
+        if not coupled:
+            st = new
+            continue
         rec = trajectory_errors(probe, new, ph, probe.eta)
         rec["alpha_gpu"], rec["alpha_oracle"] = ph["alpha"], probe.last["alpha"]
         recs.append(rec)
-        if window is not None and t >= window:
-            # beyond the conditioning window the two trajectories legitimately separate; keep
-            # them coupled for (A) by continuing the oracle from the GPU's own state
-            probe.x, probe.y, probe.z = new["x"].copy(), new["y"].copy(), new["z"].copy()
-            probe._weights()
-            st = new
-            continue
         if alphas is None:
             assert ph["alpha"] == probe.last["alpha"], f"iteration {t}: alpha gpu {ph['alpha']} vs oracle {probe.last['alpha']}"
-        for k in ("x", "y", "z"):
-            assert rec[k] <= RTOL, f"iteration {t}: B:{k} rel err {rec[k]:.3e}"
-        assert rec["wp_excess"] <= 0 and rec["wc_excess"] <= 0, f"iteration {t}: B:w beyond propagated bound {rec}"
+        if drift is not None:
+            for k in DRIFT_KEYS:
+                if k in rec:
+                    tol = drift_tol(drift, t + 1, k, factor)
+                    rec[k + "_tol"] = tol
+                    assert rec[k] <= tol, f"iteration {t}: B:{k} rel err {rec[k]:.3e} > {tol:.3e} (oracle drift {drift[t + 1].get(k):.3e})"
+        else:
+            for k in ("x", "y", "z"):
+                assert rec[k] <= RTOL, f"iteration {t}: B:{k} rel err {rec[k]:.3e}"
+            assert rec["wp_excess"] <= 0 and rec["wc_excess"] <= 0, f"iteration {t}: B:w beyond propagated bound {rec}"
         if strict_derived:   # standard step (alpha = 1) trajectories are well conditioned
             L = probe.last
             for k in ("wp", "wc", "g", "h"):
