@@ -17,6 +17,10 @@
 #include "common.cuh"
 #include "fastmath.cuh"
 
+#ifndef MWU_SEARCH_TAB
+#define MWU_SEARCH_TAB 1      // covering side of the search: table-driven (expm1, exp) pair
+#endif
+
 namespace mwu {
 
 // =====================================================================================
@@ -93,12 +97,34 @@ __device__ void stage_double_next(Ctl* c) {
 // First pass of an iteration: a window of exponents around the previous accepted step size
 // (the Table 3 caption's observation that consecutive step sizes are close, used
 // here only to choose which candidates to evaluate, not to change Alg. 3's result).
+// First pass with speculative bisection levels (PT_MIX): if the step size stays in the octave
+// [2^(ks-1), 2^ks) of the previous one, Alg. 3's doubling stops at exponent ks and its first two
+// bisection levels are already evaluated, so the iteration needs one more, small pass (the last
+// levels).  Only a choice of what to evaluate: the controller replays Alg. 3 exactly.
+__device__ void stage_mix(Ctl* c, int ks) {
+  const double b = ldexp(1.0, ks - 1);
+  const double a[MWU_MAXC] = {ldexp(1.0, ks - 2), b, 1.25 * b, 1.5 * b, 1.75 * b, ldexp(1.0, ks),
+                              ldexp(1.0, ks + 1), ldexp(1.0, ks + 2)};
+  const int e[MWU_MAXC] = {ks - 2, ks - 1, -1, -1, -1, ks, ks + 1, ks + 2};   // -1: not a doubling step
+  for (int j = 0; j < MWU_MAXC; ++j) {
+    c->cand[j] = a[j];
+    c->cexp[j] = e[j];
+    c->csq[j] = 0;
+    stage_modes(c, j);
+  }
+  c->ncand = MWU_MAXC;
+  c->ptype = PT_MIX;
+  c->pa0 = ldexp(1.0, ks - 3);
+  c->pdelta = c->pa0;
+}
+
 __device__ void stage_double_first(Ctl* c) {
   c->dk_lo = -1;
   c->dk_hi = 1 << 20;
   int kg = 1;
   if (c->t < 32 && c->aguess[c->t] >= 1.0) kg = ilogb(c->aguess[c->t]);   // previous probe, same t
   else if (c->t > 0 && c->alpha_prev >= 1.0) kg = ilogb(c->alpha_prev);
+  if (MWU_MAXC == 8 && kg + 1 >= 2 && kg + 3 < c->max_evals - 1) { stage_mix(c, kg + 1); return; }
   int k0 = kg - (MWU_MAXC / 2 - 1);
   if (k0 < 0) k0 = 0;
   int ks[MWU_MAXC];
@@ -108,7 +134,14 @@ __device__ void stage_double_first(Ctl* c) {
 
 __device__ void stage_bisect(Ctl* c) {          // the 2^L - 1 midpoints of L bisection levels
   const int Lmax = (MWU_MAXC >= 7) ? 3 : ((MWU_MAXC >= 3) ? 2 : 1);
-  const int L = c->bisect_depth < 1 ? 1 : (c->bisect_depth > Lmax ? Lmax : c->bisect_depth);
+  int L = c->bisect_depth < 1 ? 1 : (c->bisect_depth > Lmax ? Lmax : c->bisect_depth);
+  {   // no more levels than the stop rule can still ask for: lb only grows, so after l levels the
+      // bracket is (ub - lb)/2^l <= thr * lb_final once (ub - lb)/2^l <= thr * lb (Q9)
+    const double thr = c->tol_prose ? c->eps : (1.0 - c->eps);
+    int need = 1;
+    while (need < L && (c->ub - c->lb) / (double)(1 << need) > thr * c->lb) ++need;
+    L = need;
+  }
   const int n = (1 << L) - 1;
   // midpoints computed exactly as the sequential loop computes them, stored in ascending order
   double lo[8], hi[8], nlo[8], nhi[8], vals[8];
@@ -854,7 +887,6 @@ __global__ void __launch_bounds__(MWU_NT) pair_sum(int64_t E, const double* __re
 // =====================================================================================
 // Row kernels: search pass and update (P rows then C rows as one index space)
 // =====================================================================================
-constexpr size_t kSearchSmem = (size_t)MWU_SST * 3 * MWU_SCH * sizeof(double);
 
 __device__ __forceinline__ int search_slot_op(int s) {
   const int g = s / MWU_MAXC;            // 0 EP, 1 LP, 2 MX, 3 EC, 4 TC, 5 MN
@@ -875,6 +907,33 @@ struct Cands {
   int nc, pt;
   double ea0, ead;
 };
+
+// PT_MIX: expm1 at 2, 4, 5, 6, 7, 8, 16, 32 x delta from e = expm1(delta x) by exact identities
+// (doubling e(2t) = e (e + 2), grid step e(t + delta) = e + e_d + e e_d), and the same for exp
+// (q(2t) = q^2, q(t + delta) = q q_d).
+template <int NC>
+__device__ __forceinline__ void mix_chain(double ed, double (&E)[NC]) {
+  static_assert(NC == 8, "PT_MIX has 8 candidates");
+  E[0] = ed * (ed + 2.0);
+  E[1] = E[0] * (E[0] + 2.0);
+  E[2] = E[1] + ed + E[1] * ed;
+  E[3] = E[2] + ed + E[2] * ed;
+  E[4] = E[3] + ed + E[3] * ed;
+  E[5] = E[1] * (E[1] + 2.0);
+  E[6] = E[5] * (E[5] + 2.0);
+  E[7] = E[6] * (E[6] + 2.0);
+}
+template <int NC>
+__device__ __forceinline__ void mix_chain_q(double qd, double (&Q)[NC]) {
+  Q[0] = qd * qd;
+  Q[1] = Q[0] * Q[0];
+  Q[2] = Q[1] * qd;
+  Q[3] = Q[2] * qd;
+  Q[4] = Q[3] * qd;
+  Q[5] = Q[1] * Q[1];
+  Q[6] = Q[5] * Q[5];
+  Q[7] = Q[6] * Q[6];
+}
 
 // Fast per-row bodies: every candidate of the pass uses the expm1 form (Q16) on the streamed
 // side; the candidates follow from ONE transcendental per row by exact identities
@@ -898,12 +957,15 @@ struct PRowFast {
   __device__ __forceinline__ void operator()(double y, double d, double u, int64_t = 0) {
     double em = mwu_expm1(ea0 * d), emd = 0.0;
     if (PT == PT_GRID) emd = mwu_expm1(ead * d);
+    double E[NC];
+    if constexpr (PT == PT_MIX) mix_chain<NC>(em, E);
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
       if (PT == PT_DOUBLE) {
         if (SQ1) { if (j > 0) em = em * (em + 2.0); }          // consecutive exponents
         else { for (int s = 0; s < sq[j]; ++s) em = em * (em + 2.0); }
-      } else em = em + emd + em * emd;
+      } else if (PT == PT_GRID) em = em + emd + em * emd;
+      else em = E[j];
       if (lse[j]) ep[j] += mwu_exp(eta * ((y + a[j] * d) - shP[j]));   // packing side is short
       else ep[j] = __fma_rn(u, em, ep[j]);
     }
@@ -930,16 +992,26 @@ struct CRowFast {
 #pragma unroll
     for (int j = 0; j < NC; ++j) { a[j] = k.a[j]; sq[j] = k.sq[j]; ec[j] = 0.0; tc[j] = 0.0; mn[j] = INFINITY; }
   }
+  __device__ __forceinline__ void ex(double x, double& em, double& q) const {
+#if MWU_SEARCH_TAB
+    mwu_expm1_exp_tab(x, T, Mh, Ml, em, q);
+#else
+    mwu_expm1_exp(x, em, q);
+#endif
+  }
   __device__ __forceinline__ void operator()(double z, double d, double v, int64_t = 0) {
     double em, q, emd = 0.0, qd = 1.0;
-    mwu_expm1_exp(-(ea0 * d), em, q);
-    if (PT == PT_GRID) mwu_expm1_exp(-(ead * d), emd, qd);
+    ex(-(ea0 * d), em, q);
+    if (PT == PT_GRID) ex(-(ead * d), emd, qd);
+    double E[NC], Q[NC];
+    if constexpr (PT == PT_MIX) { mix_chain<NC>(em, E); mix_chain_q<NC>(q, Q); }
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
       if (PT == PT_DOUBLE) {
         if (SQ1) { if (j > 0) { em = em * (em + 2.0); q = q * q; } }
         else { for (int s = 0; s < sq[j]; ++s) { em = em * (em + 2.0); q = q * q; } }
-      } else { em = em + emd + em * emd; q = q * qd; }
+      } else if (PT == PT_GRID) { em = em + emd + em * emd; q = q * qd; }
+      else { em = E[j]; q = Q[j]; }
       ec[j] = __fma_rn(v, em, ec[j]);
       tc[j] = __fma_rn(v, q, tc[j]);
     }
@@ -958,9 +1030,11 @@ struct CRowFast {
   // masked by w1 = 0 (weight 0, z = +inf) when absent
   __device__ __forceinline__ void pair(double z0, double d0, double v0, double z1, double d1, double v1) {
     double e0, q0, e1, q1, ed0 = 0.0, qd0 = 1.0, ed1 = 0.0, qd1 = 1.0;
-    mwu_expm1_exp(-(ea0 * d0), e0, q0);
-    mwu_expm1_exp(-(ea0 * d1), e1, q1);
-    if (PT == PT_GRID) { mwu_expm1_exp(-(ead * d0), ed0, qd0); mwu_expm1_exp(-(ead * d1), ed1, qd1); }
+    ex(-(ea0 * d0), e0, q0);
+    ex(-(ea0 * d1), e1, q1);
+    if (PT == PT_GRID) { ex(-(ead * d0), ed0, qd0); ex(-(ead * d1), ed1, qd1); }
+    double E0[NC], Q0[NC], E1[NC], Q1[NC];
+    if constexpr (PT == PT_MIX) { mix_chain<NC>(e0, E0); mix_chain_q<NC>(q0, Q0); mix_chain<NC>(e1, E1); mix_chain_q<NC>(q1, Q1); }
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
       if (PT == PT_DOUBLE) {
@@ -969,9 +1043,11 @@ struct CRowFast {
         } else {
           for (int s = 0; s < sq[j]; ++s) { e0 = e0 * (e0 + 2.0); q0 = q0 * q0; e1 = e1 * (e1 + 2.0); q1 = q1 * q1; }
         }
-      } else {
+      } else if (PT == PT_GRID) {
         e0 = e0 + ed0 + e0 * ed0; q0 = q0 * qd0;
         e1 = e1 + ed1 + e1 * ed1; q1 = q1 * qd1;
+      } else {
+        e0 = E0[j]; q0 = Q0[j]; e1 = E1[j]; q1 = Q1[j];
       }
       ec[j] = __fma_rn(v1, e1, __fma_rn(v0, e0, ec[j]));
       tc[j] = __fma_rn(v1, q1, __fma_rn(v0, q0, tc[j]));
@@ -1088,6 +1164,8 @@ __device__ __forceinline__ void for_compact_rows(const double* __restrict__ rz, 
   }
 }
 
+constexpr size_t kSearchSmem = (size_t)MWU_SST * 3 * MWU_SCH * sizeof(double);
+
 struct SearchArgs {
   int64_t mP; const double *y, *dy, *u;                  // this rank's slice of the packing rows
   int64_t mC; const double *z, *dz, *v;                  // dense covering rows (v: weights)
@@ -1097,7 +1175,8 @@ struct SearchArgs {
 
 template <int PT, int NC, bool SQ1>
 __device__ __forceinline__ void search_body_fast(const SearchArgs& A, const Cands& K, const Ctl* c, double* sbuf,
-                                                 uint64_t* bars, double* part, const double* tab) {
+                                                 uint64_t* bars, double* part,
+                                                 const double* tab) {
   uint32_t it = 0;
   const int opsS[NC] = {};   // all OP_SUM (0)
   int opsX[NC], opsN[NC];
@@ -1160,14 +1239,14 @@ __global__ void __launch_bounds__(MWU_NT, MWU_SEARCH_MINB) search_pass(SearchArg
   Cands K;
   K.nc = c->ncand; K.pt = c->ptype;
   K.ea0 = c->eta * c->pa0; K.ead = c->eta * c->pdelta;
-  bool fast = (K.pt == PT_DOUBLE || K.pt == PT_GRID);
+  bool fast = (K.pt == PT_DOUBLE || K.pt == PT_GRID || (K.pt == PT_MIX && K.nc == MWU_MAXC));
   bool sq1 = true;
 #pragma unroll
   for (int j = 0; j < MWU_MAXC; ++j) {
     K.a[j] = c->cand[j]; K.ea[j] = c->cea[j]; K.shP[j] = c->shP[j]; K.shC[j] = c->shC[j];
     K.mP[j] = c->cmP[j]; K.mC[j] = c->cmC[j]; K.sq[j] = c->csq[j];
     if (j < K.nc) {
-      if (j > 0 && K.sq[j] != 1) sq1 = false;
+      if (K.pt == PT_DOUBLE && j > 0 && K.sq[j] != 1) sq1 = false;
       if (!(c->pSing || K.mP[j] == CM_EXPM1 || K.mP[j] == CM_LSE)) fast = false;
       if (!(c->cSing || K.mC[j] == CM_EXPM1)) fast = false;
     }
@@ -1191,6 +1270,7 @@ __global__ void __launch_bounds__(MWU_NT, MWU_SEARCH_MINB) search_pass(SearchArg
     MWU_FAST_CASE(PT_DOUBLE, 5, false) MWU_FAST_CASE(PT_DOUBLE, 4, false) MWU_FAST_CASE(PT_DOUBLE, 3, false)
     MWU_FAST_CASE(PT_DOUBLE, 2, false)
     MWU_FAST_CASE(PT_GRID, 7, true) MWU_FAST_CASE(PT_GRID, 3, true) MWU_FAST_CASE(PT_GRID, 1, true)
+    MWU_FAST_CASE(PT_MIX, MWU_MAXC, true)
     search_body_gen(A, K, c, sbuf, bars, part);
 #undef MWU_FAST_CASE
   } else {

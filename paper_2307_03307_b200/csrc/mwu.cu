@@ -995,7 +995,7 @@ int64_t m_total(mwu_ctx* c) { return (c->pSing ? 1 : c->mP) + (c->cSing ? 1 : (c
 void probe_begin(mwu_ctx* c, double bound, double eps) {
   if (!(eps > 0.0 && eps < 1.0)) throw MwuError{MWU_ERR_ARG, "eps must be in (0, 1)"};
   if (!(bound > 0.0) || !std::isfinite(bound)) throw MwuError{MWU_ERR_ARG, "bound must be positive and finite"};
-  if (c->n <= 0) throw MwuError{MWU_ERR_ARG, "instance has no variables"};
+  if ((c->ng > 0 ? c->ng : c->n) <= 0) throw MwuError{MWU_ERR_ARG, "instance has no variables"};   // a shard may be empty
   if (c->opt.use_graph) build_probe_graph(c);
   Ctl& h = *c->hctl;
   memset(&h, 0, sizeof(Ctl));

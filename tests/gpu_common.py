@@ -161,14 +161,19 @@ def _probe_vecs(p: O.Probe):
     return v
 
 
+SEPARATED = 1e-3      # state drift beyond which two fp64 trajectories are no longer comparable
+
+
 def self_drift(lp: O.LP, eps, alphas, iters, tol_mode="prose"):
-    """The ORACLE's own fp64 conditioning along the compared trajectory: it is rerun from x0
-    scaled by 1 +- 2^-52 (one ulp) with the same step rule, and drift[t][k] is the largest
-    elementwise relative difference (floor 1e-300) of vector k between the reruns and the
-    reference run after iteration t (t = 0: the initial state).  drift[t]["split"] is True once
-    a rerun accepted a different step size or terminated differently — a decision within the
-    rounding noise of Alg. 3 or of min z >= 1 (Q6), after which the trajectories
-    separate by the method itself.  Returns the list (length <= iters + 1)."""
+    """The ORACLE's own fp64 conditioning along the compared trajectory.  Two reruns inject one
+    ulp of rounding noise per iteration — x0 scaled by 1 + s 2^-52 and, after every update, x, y
+    and z scaled by 1 + s 2^-52 (s = +1, -1) — the size of the rounding differences any other
+    correct fp64 evaluation (other summation order, other exp) makes per iteration; drift[t][k] is
+    the largest elementwise relative difference (floor 1e-300) of vector k between the reruns and
+    the reference run after iteration t (t = 0: the initial state).  drift[t]["split"] is True
+    once a rerun accepted a different step size or terminated differently (a decision within the
+    rounding noise of Alg. 3, or of min z >= 1, Q6) or its state drifted beyond
+    SEPARATED: from there the trajectories separate by the method itself."""
     runs = [O.Probe(lp, eps, tol_mode=tol_mode)] + [O.Probe(lp, eps, tol_mode=tol_mode, x0_scale=sc)
                                                     for sc in (1 + 2.0 ** -52, 1 - 2.0 ** -52)]
 
@@ -190,7 +195,15 @@ def self_drift(lp: O.LP, eps, alphas, iters, tol_mode="prose"):
             break
         if sts[0] != O.RUNNING:                # all terminated alike: nothing more to compare
             break
-        out.append(rec(False))
+        for q, sg in zip(runs[1:], (1.0, -1.0)):
+            f = 1.0 + sg * 2.0 ** -52
+            q.x, q.y, q.z = q.x * f, q.y * f, q.z * f
+            q._weights()
+        r = rec(False)
+        if max(r["x"], r["y"], r["z"]) > SEPARATED:
+            out.append(gone)
+            break
+        out.append(r)
     return out
 
 
@@ -260,11 +273,23 @@ def lockstep(solver, probe: O.Probe, bound, eps, iters, alphas=None, phase_check
         if alphas is None:
             assert ph["alpha"] == probe.last["alpha"], f"iteration {t}: alpha gpu {ph['alpha']} vs oracle {probe.last['alpha']}"
         if drift is not None:
-            for k in DRIFT_KEYS:
-                if k in rec:
-                    tol = drift_tol(drift, t + 1, k, factor)
-                    rec[k + "_tol"] = tol
-                    assert rec[k] <= tol, f"iteration {t}: B:{k} rel err {rec[k]:.3e} > {tol:.3e} (oracle drift {drift[t + 1].get(k):.3e})"
+            for k in ("x", "y", "z", "wp", "wc", "g", "h"):
+                tol = drift_tol(drift, t + 1, k, factor)
+                rec[k + "_tol"] = tol
+                assert rec[k] <= tol, f"iteration {t}: B:{k} rel err {rec[k]:.3e} > {tol:.3e} (oracle drift {drift[t + 1].get(k):.3e})"
+            # d = sigma max(0, 1 - g/h) x: a relative error e of g/h becomes the absolute
+            # error sigma |x| (g/h) e in d (cancellation in 1 - g/h), with e bounded by the g, h
+            # bounds above plus a few ulps of the division; d^(y) = P d, d^(z) = C d inherit it
+            L = probe.last
+            x_prev = probe.x - L["alpha"] * L["d"]
+            with np.errstate(invalid="ignore", divide="ignore", over="ignore"):
+                ratio = np.where(L["h"] > 0, L["g"] / np.where(L["h"] > 0, L["h"], 1.0), 0.0)
+            e = 1e-12 + drift_tol(drift, t + 1, "g", factor) + drift_tol(drift, t + 1, "h", factor)
+            allow = e * probe.sigma * np.abs(x_prev) * np.minimum(np.abs(ratio), 2.0)
+            for k, al in (("d", allow), ("dy", probe.lp.P @ allow), ("dz", probe.lp.C @ allow)):
+                tol = drift_tol(drift, t + 1, k, factor)
+                ex = excess(ph[k], L[k], tol * np.abs(L[k]) + al)
+                assert ex <= 0, f"iteration {t}: B:{k} beyond max({tol:.2e} rel, cancellation allowance) by {ex:.3e}"
         else:
             for k in ("x", "y", "z"):
                 assert rec[k] <= RTOL, f"iteration {t}: B:{k} rel err {rec[k]:.3e}"
