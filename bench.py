@@ -61,20 +61,31 @@ def bracket(kind, gs, eps):
     raise KeyError(kind)
 
 
-def phase_bytes(kind, gs, nnz_c=None):
-    """Algorithmic (compulsory) HBM bytes per launch of each phase kernel for our data layout
-    (DESIGN.md §5): streamed arrays once, gathered vectors once (SpMV convention)."""
-    E, nv, nP = gs["E"], gs["nv"], gs["nprime"]
-    if kind == "densest":
-        return {"column": 88 * E + 8 * nP, "step": 24 * E + 16 * nP, "search": 24 * (E + nP), "update": 32 * (E + nP)}
-    if kind in ("bmatch", "match"):
-        return {"column": 40 * E + 8 * nP, "step": 16 * E + 16 * nP, "search": 24 * nP, "update": 32 * nP}
-    if kind == "vcover":
-        return {"column": 16 * E + 40 * nv, "step": 16 * E + 8 * nv, "search": 24 * E, "update": 32 * E}
-    if kind == "domset":
-        nnz = nv + 2 * E
-        return {"column": 4 * nnz + 48 * nv, "step": 4 * nnz + 24 * nv, "search": 24 * nv, "update": 32 * nv}
-    raise KeyError(kind)
+def phase_credits(kind, st):
+    """Split of the algorithmic bytes of one MWU iteration (mwu_stats.bytes_alg_per_iter
+    B_alg = S_fwd + S_tr + 32 n + 40 (m_P' + m_C')) over the phase kernels of our fused design: each
+    term goes to the ONE kernel that moves that data first, so the credits sum to B_alg exactly.
+    S = S_fwd + S_tr (structure of the four products; S_fwd = S_tr), rows: 8 B each for d^(.) write,
+    y (z) read, d^(.) read, y (z) write and the weight gather.  Embedded singleton rows cost 0.
+      densest / matching: the column kernel applies O^T / M^T AND scatters d^(y) = P d (fused),
+                          reads/writes x and d (32 n), writes d^(y) and gathers u (16 m_P), and for
+                          densest also the covering rows' z read/write, d^(z) write, v (32 m_C);
+                          search: y, d^(y) read (16 m_P) + d^(z) read (8 m_C); update: y write (8 m_P)
+      vcover / domset:    column = S/2 + 32 n + v gather (8 m_C); step (forward product + record
+                          compaction) = S/2 + d^(z) write + z read (16 m_C); search = d^(z) read
+                          (8 m_C); update = z write (8 m_C)."""
+    balg, n = st["bytes_alg_per_iter"], st["n"]
+    mP = st["m_P"] if st["m_P"] > 1 else 0          # embedded singleton rows: 0 bytes
+    mC = st["m_C"] if st["m_C"] > 1 else 0
+    S = balg - 32.0 * n - 40.0 * (mP + mC)
+    if kind in ("densest", "bmatch", "match"):
+        c = {"column": S + 32.0 * n + 16.0 * mP + 32.0 * mC, "step": 0.0, "search": 16.0 * mP + 8.0 * mC,
+             "update": 8.0 * mP}
+    else:
+        c = {"column": S / 2 + 32.0 * n + 8.0 * mC, "step": S / 2 + 16.0 * mC, "search": 8.0 * mC + 16.0 * mP,
+             "update": 8.0 * mC + 8.0 * mP}
+    assert abs(sum(c.values()) - balg) <= 1e-6 * balg, (c, balg)
+    return c
 
 
 class Clocks:
@@ -322,16 +333,21 @@ def run_ours(args):
         return 0
     value = (1 if sharded else ws) * n_done / (ms / 1000.0)
     nnz_iter = full_nnz(kind, gs)
-    pb = phase_bytes(kind, gs)
+    credit = phase_credits(kind, stats)
     peak, peak_kind = measured_peak_gbs()
     phases = {}
     for ph in ("column", "step", "search", "update"):
         p = prof[ph]
         if p["launches"] > 0 and p["ms"] > 0:
-            per_launch_ms = p["ms"] / (prof["passes"] if ph == "search" else prof["iters"])
-            phases[ph] = {"ms_per_launch": per_launch_ms, "bytes_per_launch": pb[ph],
-                          "gbs": pb[ph] / (per_launch_ms / 1000.0) / 1e9, "kernels": p["launches"]}
-    dom = max(phases, key=lambda k: phases[k]["ms_per_launch"] * (prof["passes"] / prof["iters"] if k == "search" else 1))
+            ms_iter = p["ms"] / prof["iters"]                       # all launches of the phase per iteration
+            dram, _ = ncu_traffic(args.workload, ph)                # ncu DRAM bytes per launch (committed summary)
+            per_launch = p["launches"] / prof["iters"]
+            phases[ph] = {"ms_per_iter": ms_iter, "launches_per_iter": per_launch,
+                          "alg_bytes_per_iter": credit[ph], "alg_gbs": credit[ph] / (ms_iter / 1000.0) / 1e9,
+                          "ncu_dram_bytes_per_iter": None if dram is None else dram * (prof["passes"] / prof["iters"] if ph == "search" else 1.0)}
+            if phases[ph]["ncu_dram_bytes_per_iter"] is not None:
+                phases[ph]["ncu_dram_gbs"] = phases[ph]["ncu_dram_bytes_per_iter"] / (ms_iter / 1000.0) / 1e9
+    dom = max(phases, key=lambda k: phases[k]["ms_per_iter"])
     launches_per_iter = sum(prof[p]["launches"] for p in ("column", "step", "search", "update")) / max(1, prof["iters"])
     passes_per_iter = prof["passes"] / max(1, prof["iters"])
     # whole-iteration roofline against the credited algorithmic bytes (SURVEY §8d B_alg)
@@ -384,8 +400,13 @@ def run_ours(args):
         "iteration_roofline": {"bytes_alg_per_iter": balg, "achieved_gbs": balg / (ms_per_step / 1000) / 1e9,
                                "frac_of_8TBs": balg / (ms_per_step / 1000) / 8e12,
                                "frac_of_measured": balg / (ms_per_step / 1000) / 1e9 / peak},
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": phases[dom]["gbs"], "peak": peak, "unit": "GB/s",
-                     "frac": phases[dom]["gbs"] / peak, "traffic": ncu_traffic(args.workload, dom)[0],
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": phases[dom]["alg_gbs"], "peak": peak, "unit": "GB/s",
+                     "frac": phases[dom]["alg_gbs"] / peak, "traffic": ncu_traffic(args.workload, dom)[0],
+                     "traffic_gbs": phases[dom].get("ncu_dram_gbs"),
+                     "traffic_frac": (phases[dom]["ncu_dram_gbs"] / peak) if phases[dom].get("ncu_dram_gbs") else None,
+                     "note": "achieved = the kernel's share of B_alg per iteration / its CUDA-event time (it credits x, d "
+                             "of every edge; the kernel skips those of edges inactive in this and the last step); "
+                             "traffic = ncu dram__bytes_read+write per launch",
                      "traffic_source": (ncu_traffic(args.workload, dom)[1] or {}).get("source"),
                      "peak_source": peak_kind},
         "phases": phases, "search_passes_per_iter": passes_per_iter,
@@ -395,12 +416,20 @@ def run_ours(args):
         "t_create_ms": st0["t_create_ms"], "t_generate_s": t_gen,
     }
     if args.solve:
-        S3 = Solver.graph(kind, G.src, G.dst, G.n_vertices, G.n_left if kind == "bmatch" else 0,
-                          max_iter=args.max_iter)
+        # time to (1+eps) solution (BASELINE metric): one full mwu_solve, all probes of the outer
+        # bisection, device-timed inside the library (mwu_stats.t_solve_ms; create excluded)
+        del S
+        torch.cuda.empty_cache()
+        S3 = Solver.graph(kind, G.src, G.dst, G.n_vertices, G.n_left if kind == "bmatch" else 0, **opts)
         S3.solve(eps)
         s3 = S3.stats()
-        line["time_to_solution"] = {"ms": s3["t_solve_ms"], "iters_total": s3["iters_total"], "probes": s3["probes"],
-                                    "objective": s3["objective"], "certificate": s3["certificate"]}
+        line["time_to_solution"] = {
+            "ms": s3["t_solve_ms"], "loop_ms": s3["t_loop_ms"], "iters_total": s3["iters_total"], "probes": s3["probes"],
+            "iterations_per_s": s3["iters_total"] / (s3["t_loop_ms"] / 1000.0) if s3["t_loop_ms"] > 0 else None,
+            "roofline_frac_of_8TBs": (balg * s3["iters_total"] / (s3["t_loop_ms"] / 1000.0) / 8e12) if s3["t_loop_ms"] > 0 else None,
+            "search_passes_per_iter": s3["search_passes"] / max(1, s3["iters_total"]),
+            "objective": s3["objective"], "bound": s3["bound"], "certificate": s3["certificate"],
+            "near_tie_count": s3["near_tie_count"], "t_phase_ms": s3["t_phase_ms"], "eps": eps}
     print(json.dumps(line))
     return 0
 
@@ -418,7 +447,8 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--solve", action="store_true", help="also time a full solve (time to (1+eps) solution)")
+    ap.add_argument("--no-solve", dest="solve", action="store_false",
+                    help="skip the full solve (time to (1+eps) solution), timed by default")
     ap.add_argument("--shard", action="store_true", help="sharded engine even with one rank (plumbing check)")
     ap.add_argument("--block-l", type=int, default=0, help="mwu_options.block_l (0: default L2 block shape)")
     ap.add_argument("--block-r", type=int, default=0, help="mwu_options.block_r (0: default L2 block shape)")

@@ -32,10 +32,10 @@ enum CandMode : int { CM_EXPM1 = 0, CM_LSE = 1, CM_EXT = 2 };
 // search phases (Alg. 3)
 enum SPhase : int { SP_DOUBLE = 0, SP_BISECT = 1, SP_DONE = 2, SP_FIXED = 3, SP_TCFIX = 4 };
 // candidate layout of a search pass: explicit list, doubling a0*2^j, bisection grid a0 + k*delta
-// PT_MIX (8 candidates): the doubling exponents ks-2 .. ks+2 around the predicted stopping
-// exponent ks plus the first two bisection levels of [2^(ks-1), 2^ks] (1.25, 1.5, 1.75 x 2^(ks-1)),
-// all from ONE transcendental at delta = 2^(ks-3): 2^(ks-2) = 2 delta, ..., 1.75 2^(ks-1) = 7 delta
-enum PType : int { PT_LIST = 0, PT_DOUBLE = 1, PT_GRID = 2, PT_MIX = 3 };
+// PT_G16 (8 candidates): a bisection pass over the 1/16 grid lb + j (ub - lb)/16 of the bracket
+// evaluating j = 1, 2, 4, 6, 8, 10, 12, 14 — the first three levels plus the most likely node of
+// the fourth — from TWO transcendentals (at lb + delta and delta) and a 13-step recurrence
+enum PType : int { PT_LIST = 0, PT_DOUBLE = 1, PT_GRID = 2, PT_G16 = 3 };
 
 // Finalize actions (what the last block does after a kernel's reduction).
 enum Action : int {

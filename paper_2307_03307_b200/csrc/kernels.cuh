@@ -97,39 +97,54 @@ __device__ void stage_double_next(Ctl* c) {
 // First pass of an iteration: a window of exponents around the previous accepted step size
 // (the Table 3 caption's observation that consecutive step sizes are close, used
 // here only to choose which candidates to evaluate, not to change Alg. 3's result).
-// First pass with speculative bisection levels (PT_MIX): if the step size stays in the octave
-// [2^(ks-1), 2^ks) of the previous one, Alg. 3's doubling stops at exponent ks and its first two
-// bisection levels are already evaluated, so the iteration needs one more, small pass (the last
-// levels).  Only a choice of what to evaluate: the controller replays Alg. 3 exactly.
-__device__ void stage_mix(Ctl* c, int ks) {
-  const double b = ldexp(1.0, ks - 1);
-  const double a[MWU_MAXC] = {ldexp(1.0, ks - 2), b, 1.25 * b, 1.5 * b, 1.75 * b, ldexp(1.0, ks),
-                              ldexp(1.0, ks + 1), ldexp(1.0, ks + 2)};
-  const int e[MWU_MAXC] = {ks - 2, ks - 1, -1, -1, -1, ks, ks + 1, ks + 2};   // -1: not a doubling step
-  for (int j = 0; j < MWU_MAXC; ++j) {
-    c->cand[j] = a[j];
-    c->cexp[j] = e[j];
-    c->csq[j] = 0;
-    stage_modes(c, j);
-  }
-  c->ncand = MWU_MAXC;
-  c->ptype = PT_MIX;
-  c->pa0 = ldexp(1.0, ks - 3);
-  c->pdelta = c->pa0;
-}
-
 __device__ void stage_double_first(Ctl* c) {
   c->dk_lo = -1;
   c->dk_hi = 1 << 20;
   int kg = 1;
   if (c->t < 32 && c->aguess[c->t] >= 1.0) kg = ilogb(c->aguess[c->t]);   // previous probe, same t
   else if (c->t > 0 && c->alpha_prev >= 1.0) kg = ilogb(c->alpha_prev);
-  if (MWU_MAXC == 8 && kg + 1 >= 2 && kg + 3 < c->max_evals - 1) { stage_mix(c, kg + 1); return; }
   int k0 = kg - (MWU_MAXC / 2 - 1);
   if (k0 < 0) k0 = 0;
   int ks[MWU_MAXC];
   for (int j = 0; j < MWU_MAXC; ++j) ks[j] = k0 + j;
   stage_double_exps(c, ks, MWU_MAXC);
+}
+
+// The 2^L - 1 midpoints of L bisection levels of [lb, ub], computed exactly as the sequential
+// loop computes them, ascending.
+__device__ int bisect_tree(double lb, double ub, int L, double* vals) {
+  double lo[8], hi[8], nlo[8], nhi[8];
+  int ni = 1, nv = 0;
+  lo[0] = lb; hi[0] = ub;
+  for (int lev = 0; lev < L; ++lev) {
+    int nn = 0;
+    for (int k = 0; k < ni; ++k) {
+      const double m = (lo[k] + hi[k]) / 2.0;
+      vals[nv++] = m;
+      if (lev + 1 < L) { nlo[nn] = lo[k]; nhi[nn] = m; ++nn; nlo[nn] = m; nhi[nn] = hi[k]; ++nn; }
+    }
+    for (int k = 0; k < nn; ++k) { lo[k] = nlo[k]; hi[k] = nhi[k]; }
+    ni = nn;
+  }
+  for (int i = 1; i < nv; ++i)            // insertion sort (<= 15 values)
+    for (int k = i; k > 0 && vals[k - 1] > vals[k]; --k) { const double t = vals[k]; vals[k] = vals[k - 1]; vals[k - 1] = t; }
+  return nv;
+}
+
+// A bisection that may need four levels (the stop rule of Q9 with eps < 1/8 on a whole octave):
+// one pass evaluates the first three levels and the fourth-level node of the lowest bracket
+// (the most likely of the fourth level for a log-uniform step size), so only a step size in
+// [lb + 2 delta, lb + 4 delta) needs a further, one-candidate pass.  search_controller replays
+// the sequential bisection exactly over whatever was evaluated.
+__device__ void stage_g16(Ctl* c) {
+  double v[15];
+  bisect_tree(c->lb, c->ub, 4, v);                     // v[j - 1] = lb + j (ub - lb)/16
+  const int pick[MWU_MAXC] = {1, 2, 4, 6, 8, 10, 12, 14};
+  for (int k = 0; k < MWU_MAXC; ++k) { c->cand[k] = v[pick[k] - 1]; stage_modes(c, k); }
+  c->ncand = MWU_MAXC;
+  c->ptype = PT_G16;
+  c->pdelta = (c->ub - c->lb) / 16.0;
+  c->pa0 = c->cand[0];
 }
 
 __device__ void stage_bisect(Ctl* c) {          // the 2^L - 1 midpoints of L bisection levels
@@ -139,27 +154,12 @@ __device__ void stage_bisect(Ctl* c) {          // the 2^L - 1 midpoints of L bi
       // bracket is (ub - lb)/2^l <= thr * lb_final once (ub - lb)/2^l <= thr * lb (Q9)
     const double thr = c->tol_prose ? c->eps : (1.0 - c->eps);
     int need = 1;
-    while (need < L && (c->ub - c->lb) / (double)(1 << need) > thr * c->lb) ++need;
-    L = need;
+    while (need < 4 && (c->ub - c->lb) / (double)(1 << need) > thr * c->lb) ++need;
+    if (need >= 4 && L == 3 && MWU_MAXC == 8) { stage_g16(c); return; }
+    L = need < L ? need : L;
   }
-  const int n = (1 << L) - 1;
-  // midpoints computed exactly as the sequential loop computes them, stored in ascending order
-  double lo[8], hi[8], nlo[8], nhi[8], vals[8];
-  int ni = 1, nv = 0;
-  lo[0] = c->lb; hi[0] = c->ub;
-  for (int lev = 0; lev < L; ++lev) {
-    int nn = 0;
-    for (int k = 0; k < ni; ++k) {
-      const double m = (lo[k] + hi[k]) / 2.0;
-      vals[nv++] = m;
-      nlo[nn] = lo[k]; nhi[nn] = m; ++nn;
-      nlo[nn] = m; nhi[nn] = hi[k]; ++nn;
-    }
-    for (int k = 0; k < nn; ++k) { lo[k] = nlo[k]; hi[k] = nhi[k]; }
-    ni = nn;
-  }
-  for (int i = 1; i < nv; ++i)            // insertion sort (<= 7 values)
-    for (int k = i; k > 0 && vals[k - 1] > vals[k]; --k) { const double t = vals[k]; vals[k] = vals[k - 1]; vals[k - 1] = t; }
+  double vals[8];
+  const int n = bisect_tree(c->lb, c->ub, L, vals);
   for (int k = 0; k < n; ++k) { c->cand[k] = vals[k]; stage_modes(c, k); }
   c->ncand = n;
   c->ptype = PT_GRID;
@@ -812,8 +812,8 @@ __global__ void __launch_bounds__(MWU_NT) edge_sum_compact(int64_t E64, const in
                                                            const double* __restrict__ in, double* __restrict__ out,
                                                            const double* __restrict__ z, const double* __restrict__ v,
                                                            double* __restrict__ rz, double* __restrict__ rdz,
-                                                           double* __restrict__ rv, int32_t* __restrict__ tcnt, Ctl* c,
-                                                           double* part, unsigned int* counter) {
+                                                           double* __restrict__ rv, int32_t* __restrict__ tcnt,
+                                                           int64_t rcap, Ctl* c, double* part, unsigned int* counter) {
   if (c->status != ST_RUNNING) {
     if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(c->h_search, 0u);
     return;
@@ -822,9 +822,9 @@ __global__ void __launch_bounds__(MWU_NT) edge_sum_compact(int64_t E64, const in
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ntiles = (E + MWU_CT - 1) / MWU_CT;
   double acc[3] = {-INFINITY, INFINITY, 0.0};
+  const int64_t w0 = ((int64_t)blockIdx.x * (MWU_NT / 32) + warp) * rcap;   // this warp's record stream
+  int64_t wp = w0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int seg0 = tile * MWU_CT + warp * kWarpSeg;
-    int wp = seg0;
     double s[kColEdges], zz[kColEdges], vv[kColEdges];
 #pragma unroll
     for (int k = 0; k < kColEdges; ++k) {
@@ -845,7 +845,7 @@ __global__ void __launch_bounds__(MWU_NT) edge_sum_compact(int64_t E64, const in
         if (src) out[e] = s[k];
         acc[0] = fmax(acc[0], s[k]);
         if (nz) {
-          const int p = wp + __popc(bw & ((1u << lane) - 1u));
+          const int64_t p = wp + __popc(bw & ((1u << lane) - 1u));
           rz[p] = zz[k]; rdz[p] = s[k]; rv[p] = vv[k];
         } else {
           acc[1] = fmin(acc[1], zz[k]);
@@ -854,8 +854,8 @@ __global__ void __launch_bounds__(MWU_NT) edge_sum_compact(int64_t E64, const in
       }
       wp += __popc(bw);
     }
-    if (lane == 0) tcnt[tile * (MWU_NT / 32) + warp] = wp - seg0;
   }
+  if (lane == 0) tcnt[blockIdx.x * (MWU_NT / 32) + warp] = (int32_t)(wp - w0);
   const int ops[3] = {OP_MAX, OP_MIN, OP_SUM};
   reduce_and_finalize<3>(acc, ops, part, counter, c, A_STEP_DONE_C);
 }
@@ -908,32 +908,11 @@ struct Cands {
   double ea0, ead;
 };
 
-// PT_MIX: expm1 at 2, 4, 5, 6, 7, 8, 16, 32 x delta from e = expm1(delta x) by exact identities
-// (doubling e(2t) = e (e + 2), grid step e(t + delta) = e + e_d + e e_d), and the same for exp
-// (q(2t) = q^2, q(t + delta) = q q_d).
-template <int NC>
-__device__ __forceinline__ void mix_chain(double ed, double (&E)[NC]) {
-  static_assert(NC == 8, "PT_MIX has 8 candidates");
-  E[0] = ed * (ed + 2.0);
-  E[1] = E[0] * (E[0] + 2.0);
-  E[2] = E[1] + ed + E[1] * ed;
-  E[3] = E[2] + ed + E[2] * ed;
-  E[4] = E[3] + ed + E[3] * ed;
-  E[5] = E[1] * (E[1] + 2.0);
-  E[6] = E[5] * (E[5] + 2.0);
-  E[7] = E[6] * (E[6] + 2.0);
-}
-template <int NC>
-__device__ __forceinline__ void mix_chain_q(double qd, double (&Q)[NC]) {
-  Q[0] = qd * qd;
-  Q[1] = Q[0] * Q[0];
-  Q[2] = Q[1] * qd;
-  Q[3] = Q[2] * qd;
-  Q[4] = Q[3] * qd;
-  Q[5] = Q[1] * Q[1];
-  Q[6] = Q[5] * Q[5];
-  Q[7] = Q[6] * Q[6];
-}
+// PT_G16: the candidates are lb + j delta, j = 1, 2, 4, ..., 14; expm1 and exp advance from the
+// first one by the exact identities e(t + delta) = e + ed + e ed, q(t + delta) = q qd: one step
+// to candidate 1, two steps to each later one
+template <int PT>
+__device__ __forceinline__ int grid_steps(int j) { return PT == PT_G16 ? (j == 0 ? 0 : (j == 1 ? 1 : 2)) : 1; }
 
 // Fast per-row bodies: every candidate of the pass uses the expm1 form (Q16) on the streamed
 // side; the candidates follow from ONE transcendental per row by exact identities
@@ -956,16 +935,17 @@ struct PRowFast {
   }
   __device__ __forceinline__ void operator()(double y, double d, double u, int64_t = 0) {
     double em = mwu_expm1(ea0 * d), emd = 0.0;
-    if (PT == PT_GRID) emd = mwu_expm1(ead * d);
-    double E[NC];
-    if constexpr (PT == PT_MIX) mix_chain<NC>(em, E);
+    if (PT == PT_GRID || PT == PT_G16) emd = mwu_expm1(ead * d);
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
       if (PT == PT_DOUBLE) {
         if (SQ1) { if (j > 0) em = em * (em + 2.0); }          // consecutive exponents
         else { for (int s = 0; s < sq[j]; ++s) em = em * (em + 2.0); }
       } else if (PT == PT_GRID) em = em + emd + em * emd;
-      else em = E[j];
+      else {
+#pragma unroll
+        for (int s = 0; s < grid_steps<PT>(j); ++s) em = em + emd + em * emd;
+      }
       if (lse[j]) ep[j] += mwu_exp(eta * ((y + a[j] * d) - shP[j]));   // packing side is short
       else ep[j] = __fma_rn(u, em, ep[j]);
     }
@@ -1002,16 +982,17 @@ struct CRowFast {
   __device__ __forceinline__ void operator()(double z, double d, double v, int64_t = 0) {
     double em, q, emd = 0.0, qd = 1.0;
     ex(-(ea0 * d), em, q);
-    if (PT == PT_GRID) ex(-(ead * d), emd, qd);
-    double E[NC], Q[NC];
-    if constexpr (PT == PT_MIX) { mix_chain<NC>(em, E); mix_chain_q<NC>(q, Q); }
+    if (PT == PT_GRID || PT == PT_G16) ex(-(ead * d), emd, qd);
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
       if (PT == PT_DOUBLE) {
         if (SQ1) { if (j > 0) { em = em * (em + 2.0); q = q * q; } }
         else { for (int s = 0; s < sq[j]; ++s) { em = em * (em + 2.0); q = q * q; } }
       } else if (PT == PT_GRID) { em = em + emd + em * emd; q = q * qd; }
-      else { em = E[j]; q = Q[j]; }
+      else {
+#pragma unroll
+        for (int s = 0; s < grid_steps<PT>(j); ++s) { em = em + emd + em * emd; q = q * qd; }
+      }
       ec[j] = __fma_rn(v, em, ec[j]);
       tc[j] = __fma_rn(v, q, tc[j]);
     }
@@ -1032,9 +1013,7 @@ struct CRowFast {
     double e0, q0, e1, q1, ed0 = 0.0, qd0 = 1.0, ed1 = 0.0, qd1 = 1.0;
     ex(-(ea0 * d0), e0, q0);
     ex(-(ea0 * d1), e1, q1);
-    if (PT == PT_GRID) { ex(-(ead * d0), ed0, qd0); ex(-(ead * d1), ed1, qd1); }
-    double E0[NC], Q0[NC], E1[NC], Q1[NC];
-    if constexpr (PT == PT_MIX) { mix_chain<NC>(e0, E0); mix_chain_q<NC>(q0, Q0); mix_chain<NC>(e1, E1); mix_chain_q<NC>(q1, Q1); }
+    if (PT == PT_GRID || PT == PT_G16) { ex(-(ead * d0), ed0, qd0); ex(-(ead * d1), ed1, qd1); }
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
       if (PT == PT_DOUBLE) {
@@ -1043,11 +1022,12 @@ struct CRowFast {
         } else {
           for (int s = 0; s < sq[j]; ++s) { e0 = e0 * (e0 + 2.0); q0 = q0 * q0; e1 = e1 * (e1 + 2.0); q1 = q1 * q1; }
         }
-      } else if (PT == PT_GRID) {
-        e0 = e0 + ed0 + e0 * ed0; q0 = q0 * qd0;
-        e1 = e1 + ed1 + e1 * ed1; q1 = q1 * qd1;
       } else {
-        e0 = E0[j]; q0 = Q0[j]; e1 = E1[j]; q1 = Q1[j];
+#pragma unroll
+        for (int s = 0; s < grid_steps<PT>(j); ++s) {
+          e0 = e0 + ed0 + e0 * ed0; q0 = q0 * qd0;
+          e1 = e1 + ed1 + e1 * ed1; q1 = q1 * qd1;
+        }
       }
       ec[j] = __fma_rn(v1, e1, __fma_rn(v0, e0, ec[j]));
       tc[j] = __fma_rn(v1, q1, __fma_rn(v0, q0, tc[j]));
@@ -1117,50 +1097,52 @@ struct CRowGen {
   }
 };
 
-// Compacted covering rows (fast densest path): warp per tile; the tile's records sit in
-// MWU_NT/32 per-warp segments of kWarpSeg slots with counts tcnt[tile*8 + w]; lanes walk the
-// concatenation (4 rows per lane in flight), so every lane has work whatever the segment sizes.
+// Compacted covering rows: `ns` dense record streams (one per warp of the compacting kernel),
+// stream w holding cnt[w] records (z, d^(z), v) from w * cap.  A search block takes the streams
+// w = blockIdx.x, + gridDim.x, ... and streams them through shared memory in MWU_SCH-row chunks
+// with the bulk-copy engine (the same stage ring as stream_rows3), two rows per thread at a time.
 template <class F>
-__device__ __forceinline__ void for_compact_rows(const double* __restrict__ rz, const double* __restrict__ rdz,
-                                                 const double* __restrict__ rv, const int32_t* __restrict__ tcnt,
-                                                 int64_t ntiles, F& f) {
-  constexpr int NW = MWU_NT / 32;
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * MWU_NT + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * MWU_NT) >> 5;
-  for (int64_t tile = gw; tile < ntiles; tile += nw) {
-    int cw = lane < NW ? __ldg(tcnt + tile * NW + lane) : 0;
-    int pre = cw;                                   // inclusive prefix over the NW segments
-#pragma unroll
-    for (int o = 1; o < NW; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, pre, o);
-      if (lane >= o) pre += t;
+__device__ __forceinline__ void stream_recs3(const double* rz, const double* rdz, const double* rv,
+                                             const int32_t* __restrict__ cnt, int64_t ns, int64_t cap,
+                                             double* buf, uint64_t* bars, uint32_t& it, F& f) {
+  int64_t iw = blockIdx.x, ioff = 0;               // producer cursor (thread 0)
+  int64_t cw = blockIdx.x, coff = 0;               // consumer cursor (all threads)
+  auto len = [&](int64_t w) -> int64_t { return (int64_t)__ldg(cnt + w); };
+  auto skip_empty = [&](int64_t& w, int64_t& off) {
+    while (w < ns && off >= len(w)) { w += gridDim.x; off = 0; }
+  };
+  auto issue = [&](uint32_t slot) {                // the chunk at the producer cursor
+    skip_empty(iw, ioff);
+    if (iw >= ns) return;
+    const int64_t r0 = iw * cap + ioff;
+    const int64_t rows = min((int64_t)MWU_SCH, len(iw) - ioff);
+    const uint32_t bytes = (uint32_t)(((rows * 8) + 15) & ~15ll);
+    double* s = buf + (size_t)slot * 3 * MWU_SCH;
+    mbar_expect_tx(&bars[slot], 3 * bytes);
+    const uint64_t pf = pol_first();
+    tma_load_1d_hint(s, rz + r0, bytes, &bars[slot], pf);
+    tma_load_1d_hint(s + MWU_SCH, rdz + r0, bytes, &bars[slot], pf);
+    tma_load_1d_hint(s + 2 * MWU_SCH, rv + r0, bytes, &bars[slot], pf);
+    ioff += rows;
+  };
+  if (threadIdx.x == 0)
+    for (int k = 0; k < MWU_SST; ++k) issue((it + (uint32_t)k) % MWU_SST);
+  for (;;) {
+    skip_empty(cw, coff);
+    if (cw >= ns) break;
+    const uint32_t slot = it % MWU_SST, parity = (it / MWU_SST) & 1u;
+    mbar_wait(&bars[slot], parity);
+    const int rows = (int)min((int64_t)MWU_SCH, len(cw) - coff);
+    const double* s = buf + (size_t)slot * 3 * MWU_SCH;
+    for (int r = threadIdx.x; r < rows; r += 2 * MWU_NT) {
+      const int r1 = r + MWU_NT;
+      if (r1 < rows) f.pair(s[r], s[MWU_SCH + r], s[2 * MWU_SCH + r], s[r1], s[MWU_SCH + r1], s[2 * MWU_SCH + r1]);
+      else f.pair(s[r], s[MWU_SCH + r], s[2 * MWU_SCH + r], INFINITY, 0.0, 0.0);
     }
-    int P[NW + 1];                                  // exclusive prefixes, uniform over the warp
-    P[0] = 0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) P[w + 1] = __shfl_sync(0xffffffffu, pre, w);
-    const int cnt = P[NW];
-    const int64_t base = tile * MWU_CT;
-    for (int r0 = 0; r0 < cnt; r0 += 128) {
-      double zz[4], dd[4], vv[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int r = r0 + q * 32 + lane;
-        if (r < cnt) {
-          int seg = 0, off = 0;
-#pragma unroll
-          for (int w = 1; w < NW; ++w) if (r >= P[w]) { seg = w; off = P[w]; }
-          const int64_t a = base + seg * kWarpSeg + (r - off);
-          zz[q] = __ldcs(rz + a); dd[q] = __ldcs(rdz + a); vv[q] = __ldcs(rv + a);
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 4; q += 2) {
-        const bool ok0 = r0 + q * 32 + lane < cnt, ok1 = r0 + (q + 1) * 32 + lane < cnt;
-        if (ok0) f.pair(zz[q], dd[q], vv[q], ok1 ? zz[q + 1] : INFINITY, ok1 ? dd[q + 1] : 0.0, ok1 ? vv[q + 1] : 0.0);
-      }
-    }
+    coff += rows;
+    __syncthreads();                                 // everyone is done with this slot
+    if (threadIdx.x == 0) issue(slot);
+    ++it;
   }
 }
 
@@ -1169,7 +1151,7 @@ constexpr size_t kSearchSmem = (size_t)MWU_SST * 3 * MWU_SCH * sizeof(double);
 struct SearchArgs {
   int64_t mP; const double *y, *dy, *u;                  // this rank's slice of the packing rows
   int64_t mC; const double *z, *dz, *v;                  // dense covering rows (v: weights)
-  const double *rz, *rdz, *rv; const int32_t* tcnt; int64_t ntiles;   // compacted (rz != nullptr)
+  const double *rz, *rdz, *rv; const int32_t* tcnt; int64_t nstreams, rcap;   // compacted (rz != nullptr)
   const double* emtab;                                   // 768: T, T-1 hi, T-1 lo (fastmath.cuh)
 };
 
@@ -1192,7 +1174,7 @@ __device__ __forceinline__ void search_body_fast(const SearchArgs& A, const Cand
   {
     CRowFast<PT, NC, SQ1> f(K, tab);
     if (!c->cSing) {
-      if (A.rz) for_compact_rows(A.rz, A.rdz, A.rv, A.tcnt, A.ntiles, f);
+      if (A.rz) stream_recs3(A.rz, A.rdz, A.rv, A.tcnt, A.nstreams, A.rcap, sbuf, bars, it, f);
       else stream_rows3(A.z, A.dz, A.v, A.mC, sbuf, bars, it, f);
     }
     block_partials<NC>(f.ec, opsS, part, R_EC(0));
@@ -1217,7 +1199,7 @@ __device__ __forceinline__ void search_body_gen(const SearchArgs& A, const Cands
   {
     CRowGen f(K, -c->eta);
     if (!c->cSing) {
-      if (A.rz) for_compact_rows(A.rz, A.rdz, A.rv, A.tcnt, A.ntiles, f);
+      if (A.rz) stream_recs3(A.rz, A.rdz, A.rv, A.tcnt, A.nstreams, A.rcap, sbuf, bars, it, f);
       else stream_rows3(A.z, A.dz, A.v, A.mC, sbuf, bars, it, f);
     }
     block_partials<MWU_MAXC>(f.ec, opsS, part, R_EC(0));
@@ -1239,7 +1221,7 @@ __global__ void __launch_bounds__(MWU_NT, MWU_SEARCH_MINB) search_pass(SearchArg
   Cands K;
   K.nc = c->ncand; K.pt = c->ptype;
   K.ea0 = c->eta * c->pa0; K.ead = c->eta * c->pdelta;
-  bool fast = (K.pt == PT_DOUBLE || K.pt == PT_GRID || (K.pt == PT_MIX && K.nc == MWU_MAXC));
+  bool fast = (K.pt == PT_DOUBLE || K.pt == PT_GRID || (K.pt == PT_G16 && K.nc == MWU_MAXC));
   bool sq1 = true;
 #pragma unroll
   for (int j = 0; j < MWU_MAXC; ++j) {
@@ -1270,7 +1252,7 @@ __global__ void __launch_bounds__(MWU_NT, MWU_SEARCH_MINB) search_pass(SearchArg
     MWU_FAST_CASE(PT_DOUBLE, 5, false) MWU_FAST_CASE(PT_DOUBLE, 4, false) MWU_FAST_CASE(PT_DOUBLE, 3, false)
     MWU_FAST_CASE(PT_DOUBLE, 2, false)
     MWU_FAST_CASE(PT_GRID, 7, true) MWU_FAST_CASE(PT_GRID, 3, true) MWU_FAST_CASE(PT_GRID, 1, true)
-    MWU_FAST_CASE(PT_MIX, MWU_MAXC, true)
+    MWU_FAST_CASE(PT_G16, MWU_MAXC, true)
     search_body_gen(A, K, c, sbuf, bars, part);
 #undef MWU_FAST_CASE
   } else {
@@ -1460,8 +1442,8 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
     int64_t E64, const int32_t* __restrict__ srow, const int32_t* __restrict__ drow, const double* __restrict__ u,
     double* __restrict__ x, double* __restrict__ d, double* __restrict__ z, double* __restrict__ dy,
     uint32_t* __restrict__ act, double* __restrict__ rz, double* __restrict__ rdz, double* __restrict__ rv,
-    int32_t* __restrict__ tcnt, double* gdbg, double* hdbg, Ctl* c, double* part, unsigned int* counter,
-    const double* __restrict__ exptab) {
+    int32_t* __restrict__ tcnt, int64_t rcap, double* gdbg, double* hdbg, Ctl* c, double* part,
+    unsigned int* counter, const double* __restrict__ exptab) {
   if (c->status != ST_RUNNING) return;
   __shared__ double s_tab[256];                                   // 2^(j/256), host-rounded
   s_tab[threadIdx.x] = exptab[threadIdx.x];                       // MWU_NT == 256
@@ -1486,6 +1468,10 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
   if (threadIdx.x == 0)
     for (int k = 0; k < mine && k < kColStages; ++k)
       col_issue(csm + k * kColStageBytes, &full[k], blockIdx.x + k * gridDim.x, E, z, srow, drow, act);
+  // compaction of the active covering rows: each warp appends its records to its own dense
+  // stream [w0, w0 + rcap) in (tile, k, lane) order; the count goes to tcnt at the end
+  const int64_t w0 = ((int64_t)blockIdx.x * (MWU_NT / 32) + warp) * rcap;
+  int64_t wp = w0;
   double us[kColEdges], ud[kColEdges], nus[kColEdges], nud[kColEdges];
   if (mine > 0) {
     mbar_wait(&full[0], 0u);
@@ -1519,10 +1505,6 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
       had[k] = (pw[k] >> lane) & 1u;
       if (had[k]) { xe[k] = x2[e0 + j]; dp[k] = d2[e0 + j]; }
     }
-    // compaction of the active covering rows: each warp owns the record segment
-    // [tile*CT + warp*kWarpSeg, +kWarpSeg) of its kWarpSeg edges, filled in (k, lane) order
-    const int seg0 = tile * MWU_CT + warp * kWarpSeg;
-    int wp = seg0;
 #pragma unroll
     for (int k = 0; k < kColEdges; ++k) {
       const int j = k * MWU_NT + threadIdx.x;
@@ -1558,7 +1540,7 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
         d2[e] = make_double2(d0, d1);
         const double m01 = d0 > d1 ? d0 : d1;
         maxd = m01 > maxd ? m01 : maxd;
-        const int p = wp + __popc(bw & ((1u << lane) - 1u));
+        const int64_t p = wp + __popc(bw & ((1u << lane) - 1u));
         rz[p] = zz; rdz[p] = dz; rv[p] = v;
       } else if (valid) { im = zz < im ? zz : im; is += v; }       // candidate-independent row
       wp += __popc(bw);
@@ -1574,7 +1556,6 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
     // this warp is done with the stage: release it
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[slot]);
-    if (lane == 0) tcnt[tile * (MWU_NT / 32) + warp] = wp - seg0;
     if (threadIdx.x == 0 && kt + kColStages < mine) {           // producer: refill once all warps left
       mbar_wait(&empty[slot], (uint32_t)((kt / kColStages) & 1));
       col_issue(stg, &full[slot], blockIdx.x + (kt + kColStages) * gridDim.x, E, z, srow, drow, act);
@@ -1585,6 +1566,7 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
 #pragma unroll
     for (int q = 0; q < kColEdges; ++q) { us[q] = nus[q]; ud[q] = nud[q]; }
   }
+  if (lane == 0) tcnt[blockIdx.x * (MWU_NT / 32) + warp] = (int32_t)(wp - w0);
   double acc[3] = {maxd, im, is};
   const int ops[3] = {OP_MAX, OP_MIN, OP_SUM};
   reduce_and_finalize<3>(acc, ops, part, counter, c, A_COL_FAST);

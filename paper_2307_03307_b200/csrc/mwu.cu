@@ -100,7 +100,8 @@ struct mwu_ctx {
   double* gsend = nullptr;                    // padded local slice (hooks)
   int64_t ntilesC = 0;
   double *rz = nullptr, *rdz = nullptr, *rv = nullptr;
-  int32_t* tcnt = nullptr;
+  int32_t* tcnt = nullptr;   // records per stream (one stream per warp of the compacting kernel)
+  int64_t rec_grid = 0, rec_cap = 0;   // compacting kernel's grid; records per warp stream
   uint32_t* act = nullptr;   // activity bits of d (bit e: edge e's pair of directions is nonzero)
   // vectors
   double *x = nullptr, *d = nullptr, *y = nullptr, *dy = nullptr, *u = nullptr, *z = nullptr, *dz = nullptr,
@@ -290,10 +291,14 @@ void alloc_vectors(mwu_ctx* c) {
   c->z = dalloc<double>(c, c->mC);
   if (c->lazyC || c->compC) {
     c->ntilesC = (c->mC + MWU_CT - 1) / MWU_CT;
-    c->rz = dalloc<double>(c, c->ntilesC * MWU_CT);
-    c->rdz = dalloc<double>(c, c->ntilesC * MWU_CT);
-    c->rv = dalloc<double>(c, c->ntilesC * MWU_CT);
-    c->tcnt = dalloc<int32_t>(c, c->ntilesC * (MWU_NT / 32));
+    // one dense record stream per warp of the compacting kernel (column kernel / edge_sum_compact)
+    c->rec_grid = std::max<int64_t>(1, std::min<int64_t>(c->ntilesC, (c->lazyC ? MWU_COL_MINB : 4) * (int64_t)c->sms));
+    c->rec_cap = (c->ntilesC + c->rec_grid - 1) / c->rec_grid * kWarpSeg;
+    const int64_t nrec = c->rec_grid * (MWU_NT / 32) * c->rec_cap;
+    c->rz = dalloc<double>(c, nrec);
+    c->rdz = dalloc<double>(c, nrec);
+    c->rv = dalloc<double>(c, nrec);
+    c->tcnt = dalloc<int32_t>(c, c->rec_grid * (MWU_NT / 32));
   }
   if (c->lazyC) {
     c->act = dalloc<uint32_t>(c, c->ntilesC * (MWU_CT / 32));
@@ -771,10 +776,9 @@ void enqueue_column(mwu_ctx* c, cudaStream_t st) {
     case K_DENSEST:
       if (c->lazyC) {
         CK(cudaMemsetAsync(c->dy, 0, (c->mP > 0 ? c->mP : 1) * sizeof(double), st));
-        const int64_t nt = c->ntilesC;
-        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(nt, MWU_COL_MINB * c->sms));
+        const int g = (int)c->rec_grid;
         col_densest_fast<<<g, MWU_NT, kColSmem, st>>>(c->E, c->srow, c->drow, c->u, c->x, c->d, c->z, c->dy, c->act, c->rz,
-                                              c->rdz, c->rv, c->tcnt, c->record ? c->gdbg : nullptr,
+                                              c->rdz, c->rv, c->tcnt, c->rec_cap, c->record ? c->gdbg : nullptr,
                                               c->record ? c->hdbg : nullptr, c->ctl, c->part, c->counter, c->exptab);
         inactive_exact<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, c->act, c->z, c->ctl, c->part, c->counter);
         c->launches += 2;
@@ -865,9 +869,8 @@ void enqueue_forward(mwu_ctx* c, cudaStream_t st, const double* in, double* oy, 
       break;
     case K_VCOVER:
       if (!init && c->compC) {
-        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(c->ntilesC, 4 * c->sms));
-        edge_sum_compact<<<g, MWU_NT, 0, st>>>(c->E, c->src, c->dst, in, oz, c->z, c->v, c->rz, c->rdz, c->rv,
-                                               c->tcnt, c->ctl, c->part, c->counter);
+        edge_sum_compact<<<(int)c->rec_grid, MWU_NT, 0, st>>>(c->E, c->src, c->dst, in, oz, c->z, c->v, c->rz, c->rdz,
+                                                              c->rv, c->tcnt, c->rec_cap, c->ctl, c->part, c->counter);
         inactive_exact_dz<<<rows_grid(c, c->E), MWU_NT, 0, st>>>(c->E, oz, c->z, c->ctl, c->part, c->counter);
         c->launches += 2;
         break;
@@ -883,9 +886,9 @@ void enqueue_forward(mwu_ctx* c, cudaStream_t st, const double* in, double* oy, 
             nz, c->rowidC + c->k0, c->csrC.idx + c->k0, in, oz, c->ctl, c->r0);
         c->launches++;
         if (!init && c->compC) {
-          const int g = (int)std::max<int64_t>(1, std::min<int64_t>(c->ntilesC, 4 * c->sms));
-          edge_sum_compact<<<g, MWU_NT, 0, st>>>(c->mC, nullptr, nullptr, oz, oz, c->z, c->v, c->rz, c->rdz, c->rv,
-                                                 c->tcnt, c->ctl, c->part, c->counter);
+          edge_sum_compact<<<(int)c->rec_grid, MWU_NT, 0, st>>>(c->mC, nullptr, nullptr, oz, oz, c->z, c->v, c->rz,
+                                                                c->rdz, c->rv, c->tcnt, c->rec_cap, c->ctl, c->part,
+                                                                c->counter);
           inactive_exact_dz<<<rows_grid(c, c->mC), MWU_NT, 0, st>>>(c->mC, oz, c->z, c->ctl, c->part, c->counter);
           c->launches += 2;
         } else if (!init) {
@@ -921,7 +924,8 @@ void enqueue_search(mwu_ctx* c, cudaStream_t st) {
   }
   A.mP = p1 - p0; A.y = c->y + p0; A.dy = c->dy + p0; A.u = c->u + p0;
   A.mC = c->mC; A.z = c->z; A.dz = c->dz; A.v = c->v;
-  A.rz = c->rz; A.rdz = c->rdz; A.rv = c->rv; A.tcnt = c->tcnt; A.ntiles = c->ntilesC;
+  A.rz = c->rz; A.rdz = c->rdz; A.rv = c->rv; A.tcnt = c->tcnt;
+  A.nstreams = c->rec_grid * (MWU_NT / 32); A.rcap = c->rec_cap;
   A.emtab = c->emtab;
   search_pass<<<g, MWU_NT, kSearchSmem, st>>>(A, c->ctl, c->part, c->counter);
   c->launches++;

@@ -162,18 +162,21 @@ def _probe_vecs(p: O.Probe):
 
 
 SEPARATED = 1e-3      # state drift beyond which two fp64 trajectories are no longer comparable
+NOISE = 2.0 ** -50    # rounding noise injected per iteration: 4 ulps, the typical difference a
+                      # reordered sum of a degree-16 row (or a 2-ulp exp) makes
 
 
 def self_drift(lp: O.LP, eps, alphas, iters, tol_mode="prose"):
-    """The ORACLE's own fp64 conditioning along the compared trajectory.  Two reruns inject one
-    ulp of rounding noise per iteration — x0 scaled by 1 + s 2^-52 and, after every update, x, y
-    and z scaled by 1 + s 2^-52 (s = +1, -1) — the size of the rounding differences any other
-    correct fp64 evaluation (other summation order, other exp) makes per iteration; drift[t][k] is
-    the largest elementwise relative difference (floor 1e-300) of vector k between the reruns and
-    the reference run after iteration t (t = 0: the initial state).  drift[t]["split"] is True
-    once a rerun accepted a different step size or terminated differently (a decision within the
-    rounding noise of Alg. 3, or of min z >= 1, Q6) or its state drifted beyond
-    SEPARATED: from there the trajectories separate by the method itself."""
+    """The ORACLE's own fp64 conditioning along the compared trajectory.  Two reruns inject
+    rounding noise: x0 scaled by 1 + s 2^-52 and, after every update, every element of x, y and z
+    scaled by 1 + s r NOISE (s = +1 / -1 per rerun, r = +-1 at random per element; NOISE = 4 ulps,
+    the size of the differences another correct fp64 evaluation — other summation order, other
+    exp — makes per iteration).  drift[t][k] is the largest elementwise relative difference
+    (floor 1e-300) of vector k between the reruns and the reference run after iteration t (t = 0:
+    the initial state).  drift[t]["split"] is True once a rerun accepted a different step size or
+    terminated differently (a decision within the rounding noise of Alg. 3, or of
+    min z >= 1, Q6) or its state drifted beyond SEPARATED: from there the trajectories separate by
+    the method itself."""
     runs = [O.Probe(lp, eps, tol_mode=tol_mode)] + [O.Probe(lp, eps, tol_mode=tol_mode, x0_scale=sc)
                                                     for sc in (1 + 2.0 ** -52, 1 - 2.0 ** -52)]
 
@@ -185,6 +188,7 @@ def self_drift(lp: O.LP, eps, alphas, iters, tol_mode="prose"):
                 r[k] = max(rel_err(_probe_vecs(q)[k], ref[k]) for q in runs[1:])
         return r
     out = [rec(False)]
+    rng = np.random.default_rng(12345)
     gone = {"split": True, **{k: float("inf") for k in DRIFT_KEYS}}
     for t in range(iters):
         al = None if alphas is None else alphas[t]
@@ -195,9 +199,8 @@ def self_drift(lp: O.LP, eps, alphas, iters, tol_mode="prose"):
             break
         if sts[0] != O.RUNNING:                # all terminated alike: nothing more to compare
             break
-        for q, sg in zip(runs[1:], (1.0, -1.0)):
-            f = 1.0 + sg * 2.0 ** -52
-            q.x, q.y, q.z = q.x * f, q.y * f, q.z * f
+        for q, sg in zip(runs[1:], (1.0, -1.0)):        # elementwise +-NOISE, random signs
+            q.x, q.y, q.z = (v * (1.0 + sg * NOISE * rng.choice((-1.0, 1.0), size=v.shape)) for v in (q.x, q.y, q.z))
             q._weights()
         r = rec(False)
         if max(r["x"], r["y"], r["z"]) > SEPARATED:
