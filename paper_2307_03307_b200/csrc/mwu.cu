@@ -1261,7 +1261,9 @@ void solve(mwu_ctx* c, double eps, int64_t max_iter, int32_t* outcome) {
   S.max_Px_raw = S.min_Cx_raw = S.max_Px = S.min_Cx = qnan;
   S.certificate = std::numeric_limits<double>::quiet_NaN();
   S.objective = std::numeric_limits<double>::quiet_NaN();
-  CK(cudaEventRecord(c->ev0, c->st));
+  cudaEvent_t s0, s1;                        // solve timing (run_loop uses ev0 / ev1 itself)
+  CK(cudaEventCreate(&s0)); CK(cudaEventCreate(&s1));
+  CK(cudaEventRecord(s0, c->st));
   float loop_ms_total = 0.f;
   auto run_one = [&](double B) -> int {
     probe_begin(c, B, eps);
@@ -1320,10 +1322,11 @@ void solve(mwu_ctx* c, double eps, int64_t max_iter, int32_t* outcome) {
     S.outcome = ST_FEASIBLE;
     *outcome = ST_FEASIBLE;
   }
-  CK(cudaEventRecord(c->ev1, c->st));
-  CK(cudaEventSynchronize(c->ev1));
+  CK(cudaEventRecord(s1, c->st));
+  CK(cudaEventSynchronize(s1));
   float ms = 0;
-  CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  CK(cudaEventElapsedTime(&ms, s0, s1));
+  cudaEventDestroy(s0); cudaEventDestroy(s1);
   S.t_solve_ms = ms;
   S.t_loop_ms = loop_ms_total;
   S.kernel_launches = c->launches - l0;
