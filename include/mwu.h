@@ -125,7 +125,13 @@ typedef struct {
   int compact_cover;     /* vcover / domset on one rank: the forward product compacts the covering */
                          /* rows with d^(z) > 0 for the search passes (1, default); 0 streams all  */
                          /* covering rows.  Result-neutral up to summation order.   */
+  int step_rule;         /* step size of each MWU iteration (MWU_STEP_*):                          */
+                         /*  BINARY (default) Alg. 3; NEWTON: Newton's method on        */
+                         /*  f(alpha) - 1 warm-started from the previous step, (1 - eps)^p back-off */
+                         /*  (readings Q34-Q36); STANDARD: alpha = 1 (Alg. 1) */
 } mwu_options;
+
+enum { MWU_STEP_BINARY = 0, MWU_STEP_NEWTON = 1, MWU_STEP_STANDARD = 2 };
 
 typedef struct {
   int32_t outcome, reason;           /* last probe (or solve) outcome / reason                   */

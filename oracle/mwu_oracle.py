@@ -101,6 +101,17 @@ def drop_empty_rows(A: sp.csr_matrix):
     return A[keep], keep
 
 
+def matvec(A: sp.csr_matrix, x: np.ndarray) -> np.ndarray:
+    """A x with per-row sums in CSR index order (scipy).  A matrix of ONE row — the embedded
+    objective row (1/M) 1^T of the pure modes — is a global sum over all n variables: it
+    is summed exactly rounded (math.fsum of the products), the compensated global sum of reading
+    Q22, since a sequential sum of n = 10^7 terms is off by up to n/2 ulps."""
+    if A.shape[0] == 1:
+        row = A.data * x[A.indices]
+        return np.array([math.fsum(row.tolist())])
+    return A @ x
+
+
 # --------------------------------------------------------------------------------------
 # LP instances (normalised form  Px <= 1, Cx >= 1, x >= 0 of eq:NormFeasibleLP, P:222-225)
 # --------------------------------------------------------------------------------------
@@ -344,16 +355,113 @@ def binsearch(si: SearchInputs, eps: float, tol_mode: str = "prose", max_evals: 
 
 
 # --------------------------------------------------------------------------------------
+# Newton step search (readings Q34-Q37 in DESIGN.md §3)
+# --------------------------------------------------------------------------------------
+NEWTON_MAX_STEPS = 20      # Q35: Newton steps before falling back to Alg. 3
+NEWTON_MAX_BACKOFF = 64    # Q36: at most this many (1 - eps) back-off factors
+
+
+def eta_psi_prime(si: SearchInputs, alpha: float) -> float:
+    """d/dalpha of eta*Psi(alpha) = eta <grad smax(y + alpha d^(y)), d^(y)> (P:720 differentiated):
+    eta sum_i w_i dy_i e^{eta alpha dy_i} / sum_i w_i e^{eta alpha dy_i}, evaluated with the
+    exponents shifted by their maximum.  Single packing row: eta d^(y)."""
+    if si.y.size == 1:
+        return si.eta * si.dy[0]
+    a = si.eta * alpha * si.dy
+    e = si.wp * np.exp(a - a.max())
+    return si.eta * float(np.sum(e * si.dy) / np.sum(e))
+
+
+def eta_phi_prime(si: SearchInputs, alpha: float) -> float:
+    """d/dalpha of eta*Phi(alpha) = eta <grad smin(z + alpha d^(z)), d^(z)> (P:719 differentiated):
+    eta sum_i w_i dz_i e^{-eta alpha dz_i} / sum_i w_i e^{-eta alpha dz_i}, shifted by the
+    largest exponent.  Single covering row: eta d^(z)."""
+    if si.z.size == 1:
+        return si.eta * si.dz[0]
+    a = -(si.eta * alpha) * si.dz
+    e = si.wc * np.exp(a - a.max())
+    return si.eta * float(np.sum(e * si.dz) / np.sum(e))
+
+
+def newton_search(si: SearchInputs, eps: float, alpha0: float | None, tol_mode: str = "prose",
+                  max_evals: int = 200) -> SearchResult:
+    """Newton's method on g(alpha) = f(alpha) - 1 (P:834-836): alpha <- alpha - g/g', with
+    f = Phi/Psi and g' = (Phi' Psi - Phi Psi')/Psi^2, i.e. with P = eta Phi, Q = eta Psi,
+    alpha <- alpha - (P - Q) Q / (P' Q - P Q').
+      Q34 start: the previous accepted step size; without one, Alg. 3's exponential
+          search gives the largest passing power of two (its early exit and alpha < 1 outcomes
+          are returned as Alg. 3 returns them).
+      Q35 convergence: stop at the evaluated iterate alpha once the next Newton update would move
+          it by <= eps * alpha; a non-finite or non-negative g' (f must decrease, Prop. P:746-758),
+          a non-positive update or NEWTON_MAX_STEPS steps fall back to Alg. 3 from scratch.
+      Q36 back-off: alpha <- alpha (1 - eps) until f(alpha) >= 1 (at most
+          NEWTON_MAX_BACKOFF times); the first factor tested is (1 - eps)^0.
+    Every f evaluation counts one evaluation (the derivative comes from the same pass)."""
+    evals = 0
+    if alpha0 is None or not (alpha0 >= 1.0):
+        alpha = 1.0
+        while True:                                     # Alg. 3 exponential search (P:811-817)
+            ok = f_at_least_one(si, alpha)
+            evals += 1
+            if not ok:
+                break
+            if covering_min_after(si, alpha) >= 1.0:
+                return SearchResult(alpha, evals, True)
+            if evals >= max_evals:
+                return SearchResult(alpha, evals, False)
+            alpha = 2.0 * alpha
+        if alpha == 1.0:                                # f(1) < 1: Alg. 3's own answer (< 1)
+            r = binsearch(si, eps, tol_mode, max_evals)
+            return SearchResult(r.alpha, evals + r.evals, r.early)
+        alpha0 = alpha / 2.0
+    a = float(alpha0)
+    P = Q = 0.0
+    converged = False
+    for _ in range(NEWTON_MAX_STEPS):
+        P, Q = eta_phi(si, a), eta_psi(si, a)
+        Pd, Qd = eta_phi_prime(si, a), eta_psi_prime(si, a)
+        evals += 1
+        den = Pd * Q - P * Qd
+        if not (math.isfinite(P) and math.isfinite(Q) and math.isfinite(den)) or not (den < 0.0) or not (Q > 0.0):
+            break
+        a_new = a - (P - Q) * Q / den
+        if not (math.isfinite(a_new) and a_new > 0.0):
+            break
+        if abs(a_new - a) <= eps * a:
+            converged = True
+            break
+        a = a_new
+    if not converged:                                   # Q35 fallback
+        r = binsearch(si, eps, tol_mode, max_evals)
+        return SearchResult(r.alpha, evals + r.evals, r.early)
+    ok = P >= Q                                         # f(a) >= 1, from the converged pass
+    p = 0
+    while not ok and p < NEWTON_MAX_BACKOFF:            # Q36 back-off by (1 - eps)^p
+        a = a * (1.0 - eps)
+        p += 1
+        ok = f_at_least_one(si, a)
+        evals += 1
+    return SearchResult(a, evals, False)
+
+
+# --------------------------------------------------------------------------------------
 # Alg. 2 probe: one feasibility solve of  Px <= 1, Cx >= 1  (P:651-688)
 # --------------------------------------------------------------------------------------
+STEP_RULES = ("binary", "newton", "standard")   # Alg. 3 (P:805-832) / Newton (P:834-839) / alpha = 1 (Alg. 1)
+
+
 class Probe:
-    """Alg. 2 with Alg. 3 (or a caller-supplied fixed step sequence), one iteration per
-    step() so tests can run it in lockstep with the GPU (T3 fixed-step parity)."""
+    """Alg. 2 with a step rule — Alg. 3 (default), Newton or the standard step
+    alpha = 1 of Alg. 1 ("Std" of Table 3) — or a caller-supplied fixed step
+    sequence, one iteration per step() so tests can run it in lockstep with the GPU."""
 
     def __init__(self, lp: LP, eps: float, max_iter: int = 5000, eta_factor: float = 10.0,
-                 tol_mode: str = "prose", max_evals: int = 200, x0_scale: float = 1.0):
+                 tol_mode: str = "prose", max_evals: int = 200, x0_scale: float = 1.0,
+                 step_rule: str = "binary"):
+        if step_rule not in STEP_RULES:
+            raise ValueError(step_rule)
         self.lp, self.eps, self.max_iter = lp, eps, max_iter
-        self.tol_mode, self.max_evals = tol_mode, max_evals
+        self.tol_mode, self.max_evals, self.step_rule = tol_mode, max_evals, step_rule
         self.P, self.C = lp.P, lp.C
         self.PT, self.CT = lp.P.T.tocsr(), lp.C.T.tocsr()
         self.eta = eta_parameter(lp.m, eps, eta_factor)                 # P:271 (line init2 P:656)
@@ -367,8 +475,8 @@ class Probe:
         self.x = init_x(lp.P, eps)
         if x0_scale != 1.0:   # test knob: one-ulp perturbation to measure fp sensitivity
             self.x = self.x * x0_scale
-        self.y = self.P @ self.x
-        self.z = self.C @ self.x
+        self.y = matvec(self.P, self.x)
+        self.z = matvec(self.C, self.x)
         self._weights()
         self.last: dict = {}
 
@@ -402,10 +510,17 @@ class Probe:
             self.status, self.reason = INFEASIBLE, "MAXD_ZERO"
             self.last = dict(wp=wp, wc=wc, g=g, h=h, d=d)
             return self.status
-        dy = self.P @ d
-        dz = self.C @ d
-        if alpha is None:
-            sr = binsearch(self.search_inputs(dy, dz), self.eps, self.tol_mode, self.max_evals)
+        dy = matvec(self.P, d)
+        dz = matvec(self.C, d)
+        if alpha is None and self.step_rule == "standard":
+            alpha = 1.0                                                   # Alg. 1
+        elif alpha is None:
+            si = self.search_inputs(dy, dz)
+            if self.step_rule == "newton":                                # warm start (Q34)
+                sr = newton_search(si, self.eps, self.alphas[-1] if self.alphas else None, self.tol_mode,
+                                   self.max_evals)
+            else:
+                sr = binsearch(si, self.eps, self.tol_mode, self.max_evals)
             alpha = sr.alpha
             self.evals += sr.evals
         self.last = dict(wp=wp, wc=wc, g=g, h=h, d=d, dy=dy, dz=dz, alpha=alpha)
@@ -497,12 +612,12 @@ class SolveResult:
 def solve(kind: str, src=None, dst=None, n_vertices: int = 0, eps: float = 0.1,
           max_iter: int = 5000, P: sp.csr_matrix | None = None, C: sp.csr_matrix | None = None,
           tol_mode: str = "prose", max_evals: int = 200, eta_factor: float = 10.0,
-          outer_rel_tol: float | None = None, x0_scale: float = 1.0) -> SolveResult:
+          outer_rel_tol: float | None = None, x0_scale: float = 1.0, step_rule: str = "binary") -> SolveResult:
     """Full solve: outer geometric bisection (Q14) over M (pure modes) or D (densest) with a
     fresh Alg. 2 probe per bound; IterLimit counts as infeasible.  kind in {bmatch, match,
     vcover, domset, densest, packing, covering, mixed}; the last three take explicit P / C."""
     rt = eps / 4.0 if outer_rel_tol is None else outer_rel_tol
-    kw = dict(max_iter=max_iter, eta_factor=eta_factor, tol_mode=tol_mode, max_evals=max_evals,
+    kw = dict(max_iter=max_iter, eta_factor=eta_factor, tol_mode=tol_mode, max_evals=max_evals, step_rule=step_rule,
               x0_scale=x0_scale)
     if kind == "mixed":
         p = run_probe(mixed_lp(P, C), eps, **kw)

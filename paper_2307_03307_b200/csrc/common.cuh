@@ -12,7 +12,7 @@
 
 #define MWU_NT 256            // threads per block for every kernel
 #define MWU_MAXC 8            // step-search candidates evaluated per HBM pass
-#define MWU_SLOTS 48          // reduction slots per block partial (6 * MAXC)
+#define MWU_SLOTS 50          // reduction slots per block partial (6 * MAXC + 2 Newton derivative sums)
 #ifndef MWU_CT
 #define MWU_CT 1024           // edges per column tile (compacted covering-row records)
 #endif
@@ -30,7 +30,12 @@ enum RedOp : int { OP_SUM = 0, OP_MAX = 1, OP_MIN = 2, OP_FIRST = 3 };
 // candidate evaluation modes of one side in a search pass (DESIGN.md §3 Q16)
 enum CandMode : int { CM_EXPM1 = 0, CM_LSE = 1, CM_EXT = 2 };
 // search phases (Alg. 3)
-enum SPhase : int { SP_DOUBLE = 0, SP_BISECT = 1, SP_DONE = 2, SP_FIXED = 3, SP_TCFIX = 4 };
+enum SPhase : int { SP_DOUBLE = 0, SP_BISECT = 1, SP_DONE = 2, SP_FIXED = 3, SP_TCFIX = 4,
+                    SP_NEWTON = 5, SP_NBACK = 6 };   // Newton steps, its (1 - eps)^p back-off
+// step rules (mwu_options.step_rule): Alg. 3, Newton, alpha = 1 (Alg. 1)
+enum StepRule : int { STEP_BINARY = 0, STEP_NEWTON = 1, STEP_STANDARD = 2 };
+#define MWU_NEWTON_MAX_STEPS 20     // Q35 (oracle NEWTON_MAX_STEPS)
+#define MWU_NEWTON_MAX_BACKOFF 64   // Q36 (oracle NEWTON_MAX_BACKOFF)
 // candidate layout of a search pass: explicit list, doubling a0*2^j, bisection grid a0 + k*delta
 // PT_G16 (8 candidates): a bisection pass over the 1/16 grid lb + j (ub - lb)/16 of the bracket
 // evaluating j = 1, 2, 4, 6, 8, 10, 12, 14 — the first three levels plus the most likely node of
@@ -87,6 +92,8 @@ struct Ctl {
   double mzi, Vi;                      // lazyC: inactive covering rows (d^(z) = 0): min z and
                                        // sum exp(-eta (z - mzi)) (candidate independent)
   double fixed_alpha;
+  int32_t step_rule, nk;               // step rule; Newton evaluations of this iteration
+  int32_t nfb, nb;                     // Newton fell back to Alg. 3; back-off factors applied
   int32_t ptype, pad2_;                // pass layout: PT_LIST, PT_DOUBLE (a0 2^j), PT_GRID (a0 + k delta)
   double pa0, pdelta;
   // doubling phase bookkeeping over exponents k (candidates 2^k, Alg. 3):

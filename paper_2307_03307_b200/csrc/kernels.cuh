@@ -47,6 +47,10 @@ __device__ __forceinline__ void set_cond(unsigned long long h, unsigned int v) {
 #define R_EC(j) (3 * MWU_MAXC + (j))
 #define R_TC(j) (4 * MWU_MAXC + (j))
 #define R_MN(j) (5 * MWU_MAXC + (j))
+//   NP  sum_i u_i e^{eta a0 dy_i} dy_i (candidate 0, P side; same shift as EP / LP) — Newton's Psi'
+//   NC  sum_i v_i e^{-eta a0 dz_i} dz_i (candidate 0, C side; same shift as TC)    — Newton's Phi'
+#define R_NP (6 * MWU_MAXC)
+#define R_NC (6 * MWU_MAXC + 1)
 
 __device__ void stage_modes(Ctl* c, int j) {
   c->cea[j] = c->eta * c->cand[j];
@@ -218,9 +222,88 @@ __device__ void accept_alpha(Ctl* c, double a, double mx, double mn, double tc, 
   }
 }
 
+// Newton: a pass evaluating one point a, with the derivative sums of candidate 0
+__device__ void stage_newton(Ctl* c, double a) {
+  c->cand[0] = a; c->cexp[0] = -1; c->csq[0] = 0;
+  stage_modes(c, 0);
+  c->ncand = 1; c->ptype = PT_LIST; c->sphase = SP_NEWTON; c->sactive = 1;
+}
+// the (1 - eps)^p back-off ladder after a, the multiplications done in sequence
+__device__ void stage_backoff(Ctl* c, double a) {
+  int n = MWU_MAXC;
+  if (MWU_NEWTON_MAX_BACKOFF - c->nb < n) n = MWU_NEWTON_MAX_BACKOFF - c->nb;
+  for (int j = 0; j < n; ++j) {
+    a = a * (1.0 - c->eps);
+    c->cand[j] = a; c->cexp[j] = -1; c->csq[j] = 0;
+    stage_modes(c, j);
+  }
+  c->ncand = n; c->ptype = PT_LIST; c->sphase = SP_NBACK; c->sactive = 1;
+}
+// Newton gives up (Q35): Alg. 3 from alpha = 1 with its own evaluation count
+__device__ void newton_fallback(Ctl* c) {
+  c->nfb = 1; c->evals = 0;
+  c->sphase = SP_DOUBLE;
+  stage_double_first(c);
+  c->sactive = 1;
+}
+// a candidate whose expm1 form is invalid (Q16): re-evaluate alone with the exact max / min shift
+__device__ void stage_exact_shift(Ctl* c, int j, int nP, int nC, double mxj, double mnj, int keep_phase) {
+  const double a = c->cand[j];
+  const int keepP = c->cmP[j];
+  const double kshP = c->shP[j];
+  c->cand[0] = a; c->cea[0] = c->eta * a; c->cexp[0] = -1; c->csq[0] = 0;
+  c->cmP[0] = c->pSing ? CM_EXT : (nP ? CM_LSE : keepP); c->shP[0] = nP ? mxj : kshP;
+  c->cmC[0] = c->cSing ? CM_EXT : (nC ? CM_LSE : CM_EXPM1); c->shC[0] = nC ? mnj : c->sC;
+  c->ncand = 1; c->ptype = PT_LIST; c->sphase = keep_phase; c->sactive = 1;
+}
+
+__device__ void newton_controller(Ctl* c, const double* res) {
+  if (c->sphase == SP_NEWTON) {
+    double psi, phi; int nP, nC;
+    eval_cand(c, 0, res, psi, phi, nP, nC);
+    const double mx0 = cand_mx(c, 0, res), mn0 = cand_mn(c, 0, res);
+    if (nP || nC) { stage_exact_shift(c, 0, nP, nC, mx0, mn0, SP_NEWTON); return; }
+    const double a = c->cand[0];
+    const double dphi = c->cSing ? c->eta * c->dzS : c->eta * (res[R_NC] / res[R_TC(0)]);
+    const double dpsi = c->pSing ? c->eta * c->dyS
+                                 : c->eta * (res[R_NP] / (c->cmP[0] == CM_EXPM1 ? c->SP + res[R_EP(0)] : res[R_LP(0)]));
+    c->evals++; c->evals_total++; c->nk++;
+    const double P = phi, Q = psi;
+    const double den = dphi * Q - P * dpsi;
+    bool bad = !(isfinite(P) && isfinite(Q) && isfinite(den)) || !(den < 0.0) || !(Q > 0.0);
+    double an = 0.0;
+    if (!bad) { an = a - (P - Q) * Q / den; bad = !(isfinite(an) && an > 0.0); }
+    if (bad) { newton_fallback(c); return; }
+    if (fabs(an - a) <= c->eps * a) {                       // converged (Q35): keep the evaluated a
+      if (P >= Q) { accept_alpha(c, a, mx0, mn0, cand_tc(c, 0, res), cand_sh(c, 0)); return; }
+      c->nb = 0;
+      stage_backoff(c, a);
+      return;
+    }
+    if (c->nk >= MWU_NEWTON_MAX_STEPS) { newton_fallback(c); return; }
+    stage_newton(c, an);
+    return;
+  }
+  // SP_NBACK: the ladder a (1 - eps)^p in order; the first with f >= 1, or the 64th, is the answer
+  for (int j = 0; j < c->ncand; ++j) {
+    double psi, phi; int nP, nC;
+    eval_cand(c, j, res, psi, phi, nP, nC);
+    const double mxj = cand_mx(c, j, res), mnj = cand_mn(c, j, res);
+    if (nP || nC) { stage_exact_shift(c, j, nP, nC, mxj, mnj, SP_NBACK); return; }
+    c->nb++; c->evals++; c->evals_total++;
+    if (near_tie(phi, psi)) c->near_ties++;
+    if (phi >= psi || c->nb >= MWU_NEWTON_MAX_BACKOFF) {
+      accept_alpha(c, c->cand[j], mxj, mnj, cand_tc(c, j, res), cand_sh(c, j));
+      return;
+    }
+  }
+  stage_backoff(c, c->cand[c->ncand - 1]);
+}
+
 // res layout: see R_* above
 __device__ void search_controller(Ctl* c, const double* res) {
   c->passes_total++;
+  if (c->sphase == SP_NEWTON || c->sphase == SP_NBACK) { newton_controller(c, res); return; }
   if (c->sphase == SP_FIXED) {
     accept_alpha(c, c->cand[0], cand_mx(c, 0, res), cand_mn(c, 0, res), cand_tc(c, 0, res), cand_sh(c, 0));
     return;
@@ -278,6 +361,11 @@ __device__ void search_controller(Ctl* c, const double* res) {
       const int ks = c->dk_hi;
       c->evals = ks + 1; c->evals_total += ks + 1;
       if (c->hi_exit) { accept_alpha(c, ldexp(1.0, ks), c->hi_mx, c->hi_mn, c->hi_tc, c->hi_sh); return; }
+      if (c->step_rule == STEP_NEWTON && !c->nfb && ks >= 1) {   // Newton from the largest passing 2^p (Q34)
+        c->nk = 0;
+        stage_newton(c, ldexp(1.0, ks - 1));
+        return;
+      }
       c->sphase = SP_BISECT; c->lb = ldexp(1.0, ks - 1); c->ub = ldexp(1.0, ks);
       c->lb_mx = c->ok_mx; c->lb_mn = c->ok_mn; c->lb_tc = c->ok_tc; c->lb_sh = c->ok_sh;
     } else {
@@ -377,10 +465,14 @@ __device__ void finalize(Ctl* c, int action, double* r) {
     case A_STEP_DONE + 100: {
       if (action == A_STEP_DONE + 100) c->maxdy = r[0];
       c->evals = 0;
-      if (c->fixed_alpha > 0.0) {
-        c->sphase = SP_FIXED; c->ncand = 1; c->cand[0] = c->fixed_alpha; c->ptype = PT_LIST;
-        c->cea[0] = c->eta * c->fixed_alpha; c->cmP[0] = CM_EXT; c->cmC[0] = c->lazyC ? CM_EXPM1 : CM_EXT;
+      c->nk = 0; c->nfb = 0; c->nb = 0;
+      if (c->fixed_alpha > 0.0 || c->step_rule == STEP_STANDARD) {   // fixed steps; Alg. 1's alpha = 1
+        const double fa = c->fixed_alpha > 0.0 ? c->fixed_alpha : 1.0;
+        c->sphase = SP_FIXED; c->ncand = 1; c->cand[0] = fa; c->ptype = PT_LIST;
+        c->cea[0] = c->eta * fa; c->cmP[0] = CM_EXT; c->cmC[0] = c->lazyC ? CM_EXPM1 : CM_EXT;
         c->shC[0] = c->sC;
+      } else if (c->step_rule == STEP_NEWTON && c->t > 0 && c->alpha_prev >= 1.0) {
+        stage_newton(c, c->alpha_prev);                   // warm start (Q34)
       } else {
         c->sphase = SP_DOUBLE; c->sa = 1.0;                                 // alpha <- 1
         stage_double_first(c);
@@ -889,7 +981,7 @@ __global__ void __launch_bounds__(MWU_NT) pair_sum(int64_t E, const double* __re
 // =====================================================================================
 
 __device__ __forceinline__ int search_slot_op(int s) {
-  const int g = s / MWU_MAXC;            // 0 EP, 1 LP, 2 MX, 3 EC, 4 TC, 5 MN
+  const int g = s / MWU_MAXC;            // 0 EP, 1 LP, 2 MX, 3 EC, 4 TC, 5 MN, 6 NP / NC
   return g == 2 ? OP_MAX : (g == 5 ? OP_MIN : OP_SUM);
 }
 
@@ -1049,7 +1141,8 @@ struct PRowGen {
   const Cands& k;
   double eta;
   double ep[MWU_MAXC], lp[MWU_MAXC], mx[MWU_MAXC];
-  __device__ PRowGen(const Cands& kk, double e) : k(kk), eta(e) {
+  double nd;                           // Newton: sum of the candidate-0 terms times d^(y)
+  __device__ PRowGen(const Cands& kk, double e) : k(kk), eta(e), nd(0.0) {
 #pragma unroll
     for (int j = 0; j < MWU_MAXC; ++j) { ep[j] = 0.0; lp[j] = 0.0; mx[j] = -INFINITY; }
   }
@@ -1059,8 +1152,15 @@ struct PRowGen {
       if (j < k.nc) {
         const double t = y + k.a[j] * d;
         mx[j] = fmax(mx[j], t);
-        if (k.mP[j] == CM_EXPM1) ep[j] = __fma_rn(u, expm1(k.ea[j] * d), ep[j]);
-        else if (k.mP[j] == CM_LSE) lp[j] += exp(eta * (t - k.shP[j]));
+        if (k.mP[j] == CM_EXPM1) {
+          const double em = expm1(k.ea[j] * d);
+          ep[j] = __fma_rn(u, em, ep[j]);
+          if (j == 0) nd = __fma_rn(u + u * em, d, nd);                     // u e^{eta a dy} dy
+        } else if (k.mP[j] == CM_LSE) {
+          const double e = exp(eta * (t - k.shP[j]));
+          lp[j] += e;
+          if (j == 0) nd = __fma_rn(e, d, nd);
+        }
       }
     }
   }
@@ -1074,7 +1174,8 @@ struct CRowGen {
   const Cands& k;
   double neta;
   double ec[MWU_MAXC], tc[MWU_MAXC], mn[MWU_MAXC];
-  __device__ CRowGen(const Cands& kk, double ne) : k(kk), neta(ne) {
+  double nd;                           // Newton: sum of the candidate-0 terms times d^(z)
+  __device__ CRowGen(const Cands& kk, double ne) : k(kk), neta(ne), nd(0.0) {
 #pragma unroll
     for (int j = 0; j < MWU_MAXC; ++j) { ec[j] = 0.0; tc[j] = 0.0; mn[j] = INFINITY; }
   }
@@ -1089,8 +1190,11 @@ struct CRowGen {
           expm1_exp(-(k.ea[j] * d), em, q);
           ec[j] = __fma_rn(v, em, ec[j]);
           tc[j] = __fma_rn(v, q, tc[j]);
+          if (j == 0) nd = __fma_rn(v * q, d, nd);                          // v e^{-eta a dz} dz
         } else if (k.mC[j] == CM_LSE) {
-          tc[j] += exp(neta * (t - k.shC[j]));
+          const double e = exp(neta * (t - k.shC[j]));
+          tc[j] += e;
+          if (j == 0) nd = __fma_rn(e, d, nd);
         }
       }
     }
@@ -1181,6 +1285,9 @@ __device__ __forceinline__ void search_body_fast(const SearchArgs& A, const Cand
     block_partials<NC>(f.tc, opsS, part, R_TC(0));
     block_partials<NC>(f.mn, opsN, part, R_MN(0));
   }
+  const double zero2[2] = {0.0, 0.0};
+  const int ops2[2] = {OP_SUM, OP_SUM};
+  block_partials<2>(zero2, ops2, part, R_NP);
 }
 
 __device__ __forceinline__ void search_body_gen(const SearchArgs& A, const Cands& K, const Ctl* c, double* sbuf,
@@ -1189,9 +1296,11 @@ __device__ __forceinline__ void search_body_gen(const SearchArgs& A, const Cands
   int opsS[MWU_MAXC], opsX[MWU_MAXC], opsN[MWU_MAXC];
 #pragma unroll
   for (int j = 0; j < MWU_MAXC; ++j) { opsS[j] = OP_SUM; opsX[j] = OP_MAX; opsN[j] = OP_MIN; }
+  double nd[2] = {0.0, 0.0};           // Newton derivative sums (P side, C side)
   {
     PRowGen f(K, c->eta);
     if (!c->pSing) stream_rows3(A.y, A.dy, A.u, A.mP, sbuf, bars, it, f);
+    nd[0] = f.nd;
     block_partials<MWU_MAXC>(f.ep, opsS, part, R_EP(0));
     block_partials<MWU_MAXC>(f.lp, opsS, part, R_LP(0));
     block_partials<MWU_MAXC>(f.mx, opsX, part, R_MX(0));
@@ -1205,7 +1314,9 @@ __device__ __forceinline__ void search_body_gen(const SearchArgs& A, const Cands
     block_partials<MWU_MAXC>(f.ec, opsS, part, R_EC(0));
     block_partials<MWU_MAXC>(f.tc, opsS, part, R_TC(0));
     block_partials<MWU_MAXC>(f.mn, opsN, part, R_MN(0));
+    nd[1] = f.nd;
   }
+  block_partials<2>(nd, opsS, part, R_NP);
 }
 
 // One HBM pass evaluating the staged candidates (P:716-727 on cached vectors); the

@@ -1016,6 +1016,9 @@ void probe_begin(mwu_ctx* c, double bound, double eps) {
   h.tol_prose = c->opt.tol_prose;
   h.max_evals = c->opt.max_evals;
   h.bisect_depth = c->opt.bisect_depth;
+  if (c->opt.step_rule < MWU_STEP_BINARY || c->opt.step_rule > MWU_STEP_STANDARD)
+    throw MwuError{MWU_ERR_ARG, "unknown step_rule"};
+  h.step_rule = c->opt.step_rule;
   h.use_graph = c->opt.use_graph;
   h.lazyC = c->lazyC;
   h.compC = c->compC;
@@ -1405,6 +1408,7 @@ void mwu_default_options(mwu_options* o) {
   o->block_l = 0;
   o->block_r = 0;
   o->compact_cover = 1;
+  o->step_rule = MWU_STEP_BINARY;
 }
 
 const char* mwu_last_error(const mwu_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }

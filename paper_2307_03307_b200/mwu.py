@@ -18,6 +18,7 @@ RUNNING, FEASIBLE, INFEASIBLE, ITER_LIMIT = range(4)
 OUTCOME_NAMES = {RUNNING: "running", FEASIBLE: "feasible", INFEASIBLE: "infeasible", ITER_LIMIT: "iter_limit"}
 REASON_NAMES = {0: "", 1: "MAXD_ZERO", 2: "ALPHA_LT_1", 3: "EMPTY_COVER_ROW", 4: "ITER_LIMIT", 5: "MIN_Z"}
 MIXED, PURE_PACKING, PURE_COVERING = range(3)
+STEP_RULES = {"binary": 0, "newton": 1, "standard": 2}
 GRAPH_KINDS = {"bmatch": 0, "match": 1, "vcover": 2, "domset": 3, "densest": 4}
 VEC = {"x": 0, "d": 1, "y": 2, "z": 3, "dy": 4, "dz": 5, "wp": 6, "wc": 7, "g": 8, "h": 9, "xbest": 10}
 ST = {"inc_rowptr": 0, "inc_slots": 1, "degree": 2, "prow": 3, "c_rowptr": 4, "c_colidx": 5,
@@ -46,7 +47,7 @@ class Options(ctypes.Structure):
                 ("bisect_depth", ctypes.c_int), ("device", ctypes.c_int), ("world", ctypes.c_int),
                 ("rank", ctypes.c_int), ("nccl_id", ctypes.c_void_p), ("comm_group", ctypes.c_void_p),
                 ("deterministic", ctypes.c_int), ("stream", ctypes.c_void_p), ("block_l", ctypes.c_int),
-                ("block_r", ctypes.c_int), ("compact_cover", ctypes.c_int)]
+                ("block_r", ctypes.c_int), ("compact_cover", ctypes.c_int), ("step_rule", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -138,6 +139,8 @@ def default_options(keep=None, **kw) -> Options:
             v = ctypes.cast(buf, ctypes.c_void_p)
         elif k == "comm_group" and isinstance(v, SimGroup):
             v = v.handle
+        elif k == "step_rule" and isinstance(v, str):
+            v = STEP_RULES[v]
         setattr(o, k, v)
     return o
 

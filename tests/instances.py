@@ -9,6 +9,8 @@ tools/solve_spread.py from random and structured candidates; random covering ins
 qualify (their objective <1, x_out> = rho*M carries the final iterate's chaos, ~1e-4), see
 DESIGN.md §4.
 """
+import contextlib
+
 import graphgen as gg
 
 EPS = {"bmatch": 0.1, "match": 0.1, "vcover": 0.05, "domset": 0.05, "densest": 0.1}
@@ -27,3 +29,33 @@ WELL_CONDITIONED = {
     "densest-K10,20": ("densest", lambda: gg.complete_bipartite(10, 20)),
     "densest-K15,40": ("densest", lambda: gg.complete_bipartite(15, 40)),
 }
+
+
+NOISE = 2.0 ** -50   # 4 ulps per iteration, as tests/gpu_common.self_drift
+
+
+@contextlib.contextmanager
+def rounding_noise(seed: int, noise: float = NOISE):
+    """Within this context the oracle's probes inject rounding noise after every update — every
+    element of x, y and z scaled by 1 +- noise with random signs — the size of the differences
+    another correct fp64 evaluation (other summation order, a 2-ulp exp) makes per iteration.  A
+    full solve that keeps its objective and iteration count under this noise is well conditioned
+    (test infrastructure: wraps the oracle's Probe class, no change to its arithmetic)."""
+    import numpy as np
+    import oracle.mwu_oracle as M
+    base = M.Probe
+    rng = np.random.default_rng(seed)
+
+    class Noisy(base):
+        def step(self, alpha=None):
+            st = super().step(alpha)
+            if st == M.RUNNING:
+                self.x, self.y, self.z = (v * (1.0 + noise * rng.choice((-1.0, 1.0), size=v.shape))
+                                          for v in (self.x, self.y, self.z))
+                self._weights()
+            return st
+    M.Probe = Noisy
+    try:
+        yield
+    finally:
+        M.Probe = base
