@@ -267,6 +267,54 @@ def hub_graph(n: int, hubs: int, hub_deg: int, extra: int, seed: int = 1) -> Gra
     return _finish(k // n, k % n, n, 0, f"hub({n},{hubs},{hub_deg},{extra})")
 
 
+def rgg(scale: int, avg_degree: float = 10.0, seed: int = 1) -> Graph:
+    """Random geometric graph: 2^scale points uniform in the unit square (numpy PCG64
+    `default_rng(seed)`), an edge between every pair closer than r with pi r^2 n = avg_degree —
+    the family of the paper's rgg-X inputs (e.g. rgg-18 of Table 3), which are not
+    in the container.  Edges (u < v) sorted."""
+    import numpy as np
+    n = 1 << scale
+    rng = np.random.default_rng(seed)
+    pts = rng.random((n, 2))
+    r = math.sqrt(avg_degree / (math.pi * n))
+    nc = max(1, int(1.0 / r))
+    cell = np.minimum((pts * nc).astype(np.int64), nc - 1)
+    cid = cell[:, 0] * nc + cell[:, 1]
+    order = np.argsort(cid, kind="stable")
+    cs = cid[order]
+    start = np.searchsorted(cs, np.arange(nc * nc), "left")
+    end = np.searchsorted(cs, np.arange(nc * nc), "right")
+    us, vs = [], []
+    for dx, dy in ((0, 0), (0, 1), (1, -1), (1, 0), (1, 1)):
+        tx, ty = cell[:, 0] + dx, cell[:, 1] + dy
+        ok = (tx >= 0) & (tx < nc) & (ty >= 0) & (ty < nc)
+        src = np.nonzero(ok)[0]
+        t = tx[src] * nc + ty[src]
+        cnt = end[t] - start[t]
+        rep_src = np.repeat(src, cnt)
+        offs = np.arange(cnt.sum()) - np.repeat(np.cumsum(cnt) - cnt, cnt)
+        dst = order[np.repeat(start[t], cnt) + offs]
+        keep = (np.sum((pts[rep_src] - pts[dst]) ** 2, axis=1) < r * r) & (rep_src != dst)
+        if dx == 0 and dy == 0:
+            keep &= rep_src < dst
+        us.append(rep_src[keep])
+        vs.append(dst[keep])
+    u, v = np.concatenate(us), np.concatenate(vs)
+    a, b = np.minimum(u, v), np.maximum(u, v)
+    k = np.unique(a * n + b)
+    return _finish(torch.from_numpy(k // n), torch.from_numpy(k % n), n, 0, f"rgg-{scale}")
+
+
+def biadjacency(g: Graph) -> Graph:
+    """Bipartite graph read from the adjacency matrix of g (rows = left copy, columns = right copy):
+    the paper's bmatch reading of a general matrix; both directions of every edge."""
+    n = g.n_vertices
+    a = torch.cat([g.src, g.dst]).to(torch.int64)
+    b = torch.cat([g.dst, g.src]).to(torch.int64) + n
+    k, _ = torch.sort(a * (2 * n) + b)
+    return _finish(k // (2 * n), k % (2 * n), 2 * n, n, f"biadj({g.name})")
+
+
 def disjoint_union(*graphs: Graph) -> Graph:
     """Vertex-disjoint union, edges in the order of the parts (ids shifted per part)."""
     src, dst, off = [], [], 0

@@ -151,8 +151,8 @@ def test_sharded_fixed_steps_match_oracle(cuda_ok, world, ci):
             assert np.array_equal(o[k], outs[0][k])          # every rank holds the same vectors
 
 
-SHARDED_WELL = ["bmatch-bu21", "match-er21", "vcover-S50+K8,12", "domset-K25,26", "domset-K20,30+5",
-                "densest-K10,20"]
+SHARDED_WELL = ["bmatch-bu21", "match-er21", "vcover-K5,200", "domset-K25,26", "domset-K20,30+5",
+                "densest-er400s204"]
 
 
 @pytest.mark.gpu

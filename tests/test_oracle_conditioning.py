@@ -3,7 +3,7 @@ precondition under which BASELINE's full-run tolerances can be asserted for the 
 import pytest
 
 import oracle as O
-from instances import EPS, MAX_ITER, WELL_CONDITIONED
+from instances import EPS, MAX_ITER, WELL_CONDITIONED, rounding_noise
 
 
 @pytest.mark.parametrize("name", sorted(WELL_CONDITIONED))
@@ -13,6 +13,9 @@ def test_well_conditioned_full_solve(name):
     s, d = G.numpy()
     runs = [O.solve(kind, s, d, G.n_vertices, eps=EPS[kind], max_iter=MAX_ITER, x0_scale=sc)
             for sc in (1.0, 1 + 2.0 ** -52, 1 - 2.0 ** -52)]
+    for seed in (1, 2, 3):
+        with rounding_noise(seed):
+            runs.append(O.solve(kind, s, d, G.n_vertices, eps=EPS[kind], max_iter=MAX_ITER))
     r = runs[0]
     assert r.iters_total > 0
     for q in runs:
