@@ -479,6 +479,7 @@ class Probe:
         self.z = matvec(self.C, self.x)
         self._weights()
         self.last: dict = {}
+        self.perturb = None   # test knob: callable (g, h) -> (g, h), rounding-noise models
 
     def _weights(self):
         self.sP, self.u, self.SP = shifted_weights_packing(self.y, self.eta)
@@ -505,6 +506,8 @@ class Probe:
         wc = self.v / self.SC                                             # grad smin(z)
         g = self.PT @ wp
         h = self.CT @ wc
+        if self.perturb is not None:
+            g, h = self.perturb(g, h)
         d = direction(g, h, self.x, self.sigma)
         if d.size == 0 or d.max() == 0.0:
             self.status, self.reason = INFEASIBLE, "MAXD_ZERO"

@@ -168,15 +168,16 @@ NOISE = 2.0 ** -50    # rounding noise injected per iteration: 4 ulps, the typic
 
 def self_drift(lp: O.LP, eps, alphas, iters, tol_mode="prose"):
     """The ORACLE's own fp64 conditioning along the compared trajectory.  Two reruns inject
-    rounding noise: x0 scaled by 1 + s 2^-52 and, after every update, every element of x, y and z
-    scaled by 1 + s r NOISE (s = +1 / -1 per rerun, r = +-1 at random per element; NOISE = 4 ulps,
-    the size of the differences another correct fp64 evaluation — other summation order, other
-    exp — makes per iteration).  drift[t][k] is the largest elementwise relative difference
-    (floor 1e-300) of vector k between the reruns and the reference run after iteration t (t = 0:
-    the initial state).  drift[t]["split"] is True once a rerun accepted a different step size or
-    terminated differently (a decision within the rounding noise of Alg. 3, or of
-    min z >= 1, Q6) or its state drifted beyond SEPARATED: from there the trajectories separate by
-    the method itself."""
+    rounding noise of the size another correct fp64 evaluation makes (other summation order, a
+    2-ulp exp): x0 scaled by 1 + s 2^-52; every element of g = P^T w_p and h = C^T w_c scaled by
+    1 + s r NOISE before the direction is formed (so the noise passes through the cancellation in
+    1 - g/h as the GPU's does); and every element of x, y, z scaled likewise after each update
+    (s = +1 / -1 per rerun, r = +-1 at random per element, NOISE = 4 ulps).  drift[t][k] is the
+    largest elementwise relative difference (floor 1e-300) of vector k between the reruns and the
+    reference run after iteration t (t = 0: the initial state).  drift[t]["split"] is True once a
+    rerun accepted a different step size or terminated differently (a decision within the
+    rounding noise of Alg. 3, or of min z >= 1, Q6) or its state drifted beyond
+    SEPARATED: from there the trajectories separate by the method itself."""
     runs = [O.Probe(lp, eps, tol_mode=tol_mode)] + [O.Probe(lp, eps, tol_mode=tol_mode, x0_scale=sc)
                                                     for sc in (1 + 2.0 ** -52, 1 - 2.0 ** -52)]
 
@@ -187,8 +188,11 @@ def self_drift(lp: O.LP, eps, alphas, iters, tol_mode="prose"):
             if k in ref:
                 r[k] = max(rel_err(_probe_vecs(q)[k], ref[k]) for q in runs[1:])
         return r
-    out = [rec(False)]
     rng = np.random.default_rng(12345)
+    for q, sg in zip(runs[1:], (1.0, -1.0)):      # +-NOISE on every element of g and h, random signs
+        q.perturb = (lambda g, h, sg=sg: (g * (1.0 + sg * NOISE * rng.choice((-1.0, 1.0), size=g.shape)),
+                                          h * (1.0 + sg * NOISE * rng.choice((-1.0, 1.0), size=h.shape))))
+    out = [rec(False)]
     gone = {"split": True, **{k: float("inf") for k in DRIFT_KEYS}}
     for t in range(iters):
         al = None if alphas is None else alphas[t]
