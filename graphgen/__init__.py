@@ -10,5 +10,5 @@ from .generators import (  # noqa: F401
     complete_graph, complete_bipartite, star_graph, path_graph, cycle_graph,
     circulant_regular, random_small_graph, hub_graph, random_small_bipartite,
     random_planted_lp, infeasible_lp, config_graph, CONFIGS, disjoint_union, plus_random_edges,
-    rgg, biadjacency,
+    rgg, biadjacency, gmatch_instance,
 )

@@ -315,6 +315,33 @@ def biadjacency(g: Graph) -> Graph:
     return _finish(k // (2 * n), k % (2 * n), 2 * n, n, f"biadj({g.name})")
 
 
+def gmatch_instance(n_users: int, n_items: int, seed: int = 1, deg_lo: int = 10, deg_hi: int = 40,
+                    s: float = 1.0, user_bounds=(3.0, 5.0), item_ub: float = 200.0):
+    """Synthetic generalized-matching instance shaped like the paper's App. A.2 preprocessing of
+    the Netflix / KDD ratings graphs (the datasets are not in the container): a
+    bipartite users x items graph, every user with deg_lo..deg_hi ratings (users with < 10 are
+    excluded there) of items drawn with Zipf(s) popularity, bounds lb = 3, ub = 5 per user and
+    no lower, upper item_ub per item.  Returns (Graph, lb, ub) with float64 bound tensors."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    w = 1.0 / np.arange(1, n_items + 1) ** s
+    w /= w.sum()
+    src, dst = [], []
+    for u in range(n_users):
+        k = int(rng.integers(deg_lo, deg_hi + 1))
+        items = rng.choice(n_items, size=min(k, n_items), replace=False, p=w)
+        src.extend([u] * len(items))
+        dst.extend((n_users + items).tolist())
+    o = np.lexsort((np.asarray(dst), np.asarray(src)))
+    g = Graph(torch.tensor(np.asarray(src)[o], dtype=torch.int32), torch.tensor(np.asarray(dst)[o], dtype=torch.int32),
+              n_users + n_items, n_users, f"gm({n_users},{n_items},{seed})")
+    lb = torch.zeros(n_users + n_items, dtype=torch.float64)
+    ub = torch.full((n_users + n_items,), float(item_ub), dtype=torch.float64)
+    lb[:n_users] = user_bounds[0]
+    ub[:n_users] = user_bounds[1]
+    return g, lb, ub
+
+
 def disjoint_union(*graphs: Graph) -> Graph:
     """Vertex-disjoint union, edges in the order of the parts (ids shifted per part)."""
     src, dst, off = [], [], 0

@@ -209,6 +209,18 @@ mwu_status mwu_create_csr(const mwu_csr *P, const mwu_csr *C, mwu_mode mode,
  * self-loops, duplicate edges, BMATCH endpoints not split by n_left. */
 mwu_status mwu_create_graph(const mwu_graph *g, const mwu_options *opt, mwu_ctx **out);
 
+/* Generalized matching: the mixed feasibility LP
+ * l <= M x <= u, x >= 0 over the edge variables of g (M = vertex-edge incidence, eq:incidence), as
+ * P = diag(1/u) M (rows of the vertices with finite u) and C = diag(1/l) M (rows with l > 0), both
+ * built on device from the vertex -> incident-edge CSR, then solved by the explicit-CSR engine as
+ * one MIXED probe (mwu_solve; x indexed by edge id, Q29).  lb, ub: [n_vertices] doubles, host or
+ * device, borrowed; need 0 <= lb <= ub, ub > 0 (+inf = no upper bound), lb finite.  Errors
+ * (MWU_ERR_ARG): graph errors as mwu_create_graph, bad bounds, no finite u or no positive l, an
+ * edge with both endpoints unbounded above (x_e unbounded).  A vertex with l > 0 and no edges makes
+ * the LP infeasible (solve returns INFEASIBLE / EMPTY_COVER_ROW). */
+mwu_status mwu_create_gmatch(const mwu_graph *g, const double *lb, const double *ub, const mwu_options *opt,
+                             mwu_ctx **out);
+
 /* Full solve: outer geometric bisection over the bound (Q14) with a fresh Alg. 2 probe per
  * bound (pure modes / DENSEST), or a single probe (MIXED CSR).  max_iter <= 0 keeps the option.
  * *outcome receives the outcome (pure modes always end FEASIBLE with the best certified x or the

@@ -147,6 +147,27 @@ def mixed_lp(P: sp.csr_matrix, C: sp.csr_matrix) -> LP:
     return LP(P2, C.tocsr(), MIXED, keep)
 
 
+def gmatch_matrices(src, dst, n_vertices: int, lb, ub):
+    """Generalized matching l <= M x <= u in the normalised form of eq:NormFeasibleLP:
+    P = diag(1/u) M over the vertices with finite u, C = diag(1/l) M over the vertices with l > 0
+    (rows in vertex order, M = eq:incidence)."""
+    lb = np.asarray(lb, dtype=np.float64)
+    ub = np.asarray(ub, dtype=np.float64)
+    M = incidence_M(src, dst, n_vertices)
+    pr = np.flatnonzero(np.isfinite(ub))
+    cr = np.flatnonzero(lb > 0)
+    P = (sp.diags(1.0 / ub[pr]) @ M[pr]).tocsr()
+    C = (sp.diags(1.0 / lb[cr]) @ M[cr]).tocsr()
+    P.sort_indices()
+    C.sort_indices()
+    return P, C
+
+
+def gmatch_lp(src, dst, n_vertices: int, lb, ub) -> LP:
+    """Generalized matching as a mixed LP (empty packing rows dropped, Q17)."""
+    return mixed_lp(*gmatch_matrices(src, dst, n_vertices, lb, ub))
+
+
 def densest_lp(src, dst, n_vertices: int, D: float) -> LP:
     """Feasibility form of the densest-subgraph dual (eq:densest_linalg):
     W z >= 1, O z <= D 1, i.e. P = (1/D) O, C = W (mixed)."""

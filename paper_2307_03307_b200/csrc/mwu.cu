@@ -723,6 +723,106 @@ void compact_rows(mwu_ctx* c, Seg& S) {
   tfree(scan);
 }
 
+// packing side of an explicit instance, after csrP holds the CSR: drop empty rows (Q17), tile
+// plan, CSC copy, column maxima ||P_{:,i}||_inf for x0
+void finish_csr_packing(mwu_ctx* c, int64_t n) {
+  compact_rows(c, c->csrP);                       // Q17
+  c->mP = c->csrP.nrows; c->nnzP = c->csrP.nnz;
+  build_plan(c, c->csrP);
+  build_csc(c, c->csrP, n, c->cscP);
+  c->colmaxP = dalloc<double>(c, n);
+  c->crecipP = dalloc<double>(c, n);
+  k_col_stats<<<grid_for(c, n), MWU_NT, 0, c->st>>>(n, c->cscP.rowptr, c->cscP.val, c->colmaxP, nullptr, c->crecipP);
+  CKL();
+  // an all-zero packing column leaves x_i = eps/(n*0) undefined
+  double* mn = talloc<double>(1);
+  size_t tb = 0;
+  CK(cub::DeviceReduce::Min(nullptr, tb, c->colmaxP, mn, n, c->st));
+  void* t = talloc<char>(tb);
+  CK(cub::DeviceReduce::Min(t, tb, c->colmaxP, mn, n, c->st));
+  const double mincol = read_scalar(c, mn);
+  tfree(t); tfree(mn);
+  if (!(mincol > 0.0)) throw MwuError{MWU_ERR_ARG, "P has an all-zero column: initialisation x_i = eps/(n ||P_:,i||) undefined"};
+}
+
+// covering side: record empty covering rows (infeasible, Q17), tile plan, CSC copy, column sums
+void finish_csr_covering(mwu_ctx* c, int64_t n) {
+  c->mC = c->csrC.nrows; c->nnzC = c->csrC.nnz;
+  // empty covering rows make the LP infeasible (0 >= 1), Q17
+  {
+    Seg tmpS = c->csrC;
+    const int64_t before = tmpS.nrows;
+    int64_t saved = c->empty_dropped;
+    compact_rows(c, tmpS);
+    c->empty_cover = (tmpS.nrows != before);
+    c->empty_dropped = saved;
+  }
+  build_plan(c, c->csrC);
+  build_csc(c, c->csrC, n, c->cscC);
+  c->colsumC = dalloc<double>(c, n);
+  c->crecipC = dalloc<double>(c, n);
+  k_col_stats<<<grid_for(c, n), MWU_NT, 0, c->st>>>(n, c->cscC.rowptr, c->cscC.val, nullptr, c->colsumC, c->crecipC);
+  CKL();
+}
+
+// Generalized matching (NEXT#3): rows of diag(1/b) M for the vertices selected by
+// sel (the vertex -> incident-slot CSR gives each row's edges in ascending edge id: canonical CSR)
+__global__ void k_gm_count(int64_t nrows, const int32_t* __restrict__ sel, const int64_t* __restrict__ inc_rowptr,
+                           int64_t* __restrict__ cnt) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = sel[r];
+    cnt[r] = inc_rowptr[v + 1] - inc_rowptr[v];
+  }
+}
+__global__ void k_gm_fill(int64_t nrows, const int32_t* __restrict__ sel, const int64_t* __restrict__ inc_rowptr,
+                          const uint32_t* __restrict__ slots, const double* __restrict__ bound,
+                          const int64_t* __restrict__ rowptr, uint32_t* __restrict__ col, double* __restrict__ val) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = sel[r];
+    const double w = 1.0 / bound[v];                    // row v of M scaled by 1/u(v) or 1/l(v)
+    const int64_t a = inc_rowptr[v], b = inc_rowptr[v + 1], o = rowptr[r];
+    for (int64_t k = a; k < b; ++k) { col[o + (k - a)] = slots[k] >> 1; val[o + (k - a)] = w; }
+  }
+}
+__global__ void k_gm_flags(int64_t nv, const double* __restrict__ lb, const double* __restrict__ ub,
+                           uint8_t* __restrict__ fp, uint8_t* __restrict__ fc, unsigned int* __restrict__ err) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+    const double l = lb[v], u = ub[v];
+    if (!(l >= 0.0) || !(u > 0.0) || !(l <= u) || isinf(l)) atomicOr(err, 64u);
+    fp[v] = isfinite(u) ? 1 : 0;                         // packing row  (1/u(v)) M_v x <= 1
+    fc[v] = (l > 0.0) ? 1 : 0;                           // covering row (1/l(v)) M_v x >= 1
+  }
+}
+
+// select the flagged vertex ids, build the scaled CSR of their incidence rows
+void build_gm_side(mwu_ctx* c, const uint8_t* flags, const double* bound, Seg& S) {
+  const int64_t nv = c->nv;
+  int32_t* sel = talloc<int32_t>(nv);
+  int64_t* nsel = talloc<int64_t>(1);
+  cub::CountingInputIterator<int32_t> it(0);
+  size_t tb = 0;
+  CK(cub::DeviceSelect::Flagged(nullptr, tb, it, flags, sel, nsel, nv, c->st));
+  void* t = talloc<char>(tb);
+  CK(cub::DeviceSelect::Flagged(t, tb, it, flags, sel, nsel, nv, c->st));
+  const int64_t rows = read_scalar(c, nsel);
+  tfree(t);
+  S.nrows = rows;
+  S.rowptr = dalloc<int64_t>(c, rows + 1);
+  int64_t* cnt = talloc<int64_t>(rows);
+  if (rows > 0) { k_gm_count<<<grid_for(c, rows), MWU_NT, 0, c->st>>>(rows, sel, c->inc_all.rowptr, cnt); CKL(); }
+  exclusive_scan_total(c, cnt, S.rowptr, rows);
+  S.nnz = read_scalar(c, S.rowptr + rows);
+  S.idx = dalloc<uint32_t>(c, S.nnz);
+  S.val = dalloc<double>(c, S.nnz);
+  if (rows > 0) {
+    k_gm_fill<<<grid_for(c, rows), MWU_NT, 0, c->st>>>(rows, sel, c->inc_all.rowptr, c->inc_all.idx, bound, S.rowptr,
+                                                      S.idx, S.val);
+    CKL();
+  }
+  sync(c);
+  tfree(cnt); tfree(sel); tfree(nsel);
+}
+
 // ------------------------------------------------------------------------------ kernel launchers
 template <class Ep>
 void launch_seg(mwu_ctx* c, cudaStream_t st, const Seg& S, ItemGather it, Ep ep, int action) {
@@ -1492,6 +1592,63 @@ mwu_status mwu_create_graph(const mwu_graph* g, const mwu_options* opt, mwu_ctx*
   return MWU_OK;
 }
 
+mwu_status mwu_create_gmatch(const mwu_graph* g, const double* lb, const double* ub, const mwu_options* opt,
+                             mwu_ctx** out) {
+  if (!out) return MWU_ERR_ARG;
+  *out = nullptr;
+  if (!g || !lb || !ub || g->n_vertices <= 0 || g->n_edges <= 0 || !g->src || !g->dst || g->n_vertices > INT32_MAX ||
+      g->n_edges > INT32_MAX) {
+    g_create_err = "mwu_create_gmatch: bad descriptor or bounds";
+    return MWU_ERR_ARG;
+  }
+  mwu_ctx* c = new mwu_ctx();
+  try {
+    init_ctx_common(c, opt);
+    if (c->world > 1 || c->sharded) throw MwuError{MWU_ERR_ARG, "generalized matching runs on one rank"};
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
+    CK(cudaEventRecord(a, c->st));
+    mwu_graph gv = *g;
+    gv.kind = MWU_G_VCOVER;                    // validation + vertex -> incident-slot CSR (sorted slots)
+    build_graph_storage(c, &gv);
+    const int64_t nv = c->nv, E = c->E;
+    double* dlb = dalloc<double>(c, nv);
+    double* dub = dalloc<double>(c, nv);
+    CK(cudaMemcpyAsync(dlb, lb, nv * sizeof(double), cudaMemcpyDefault, c->st));
+    CK(cudaMemcpyAsync(dub, ub, nv * sizeof(double), cudaMemcpyDefault, c->st));
+    uint8_t* fp = talloc<uint8_t>(nv);
+    uint8_t* fc = talloc<uint8_t>(nv);
+    unsigned int* err = talloc<unsigned int>(1);
+    CK(cudaMemsetAsync(err, 0, sizeof(unsigned int), c->st));
+    k_gm_flags<<<grid_for(c, nv), MWU_NT, 0, c->st>>>(nv, dlb, dub, fp, fc, err);
+    CKL();
+    const unsigned int eb = read_scalar(c, err);
+    tfree(err);
+    if (eb) throw MwuError{MWU_ERR_ARG, "mwu_create_gmatch: need 0 <= lb <= ub, ub > 0, lb finite"};
+    c->kind = K_CSR; c->mode = MWU_MIXED; c->n = E;
+    build_gm_side(c, fp, dub, c->csrP);        // P = diag(1/u) M over the vertices with finite u
+    build_gm_side(c, fc, dlb, c->csrC);        // C = diag(1/l) M over the vertices with l > 0
+    tfree(fp); tfree(fc);
+    if (c->csrP.nrows == 0 || c->csrC.nrows == 0)
+      throw MwuError{MWU_ERR_ARG, "mwu_create_gmatch: needs a finite upper bound and a positive lower bound somewhere"};
+    finish_csr_packing(c, E);
+    finish_csr_covering(c, E);
+    alloc_vectors(c);
+    fill_static_stats(c);
+    CK(cudaEventRecord(b, c->st));
+    CK(cudaEventSynchronize(b));
+    float ms = 0; CK(cudaEventElapsedTime(&ms, a, b));
+    c->stats.t_create_ms = ms;
+    cudaEventDestroy(a); cudaEventDestroy(b);
+  } catch (const MwuError& e) {
+    g_create_err = e.msg;
+    destroy_ctx(c);
+    return e.st;
+  }
+  *out = c;
+  return MWU_OK;
+}
+
 mwu_status mwu_create_csr(const mwu_csr* P, const mwu_csr* C, mwu_mode mode, const mwu_options* opt, mwu_ctx** out) {
   if (!out) return MWU_ERR_ARG;
   *out = nullptr;
@@ -1513,46 +1670,13 @@ mwu_status mwu_create_csr(const mwu_csr* P, const mwu_csr* C, mwu_mode mode, con
     c->kind = K_CSR; c->mode = mode; c->n = n;
     if (needP) {
       copy_csr_checked(c, P, c->csrP, n, "P");
-      compact_rows(c, c->csrP);                       // Q17
-      c->mP = c->csrP.nrows; c->nnzP = c->csrP.nnz;
-      build_plan(c, c->csrP);
-      build_csc(c, c->csrP, n, c->cscP);
-      c->colmaxP = dalloc<double>(c, n);
-      c->crecipP = dalloc<double>(c, n);
-      k_col_stats<<<grid_for(c, n), MWU_NT, 0, c->st>>>(n, c->cscP.rowptr, c->cscP.val, c->colmaxP, nullptr, c->crecipP);
-      CKL();
-      double s, mx;
-      // an all-zero packing column leaves x_i = eps/(n*0) undefined
-      double* mn = talloc<double>(1);
-      size_t tb = 0;
-      CK(cub::DeviceReduce::Min(nullptr, tb, c->colmaxP, mn, n, c->st));
-      void* t = talloc<char>(tb);
-      CK(cub::DeviceReduce::Min(t, tb, c->colmaxP, mn, n, c->st));
-      const double mincol = read_scalar(c, mn);
-      tfree(t); tfree(mn);
-      (void)s; (void)mx;
-      if (!(mincol > 0.0)) throw MwuError{MWU_ERR_ARG, "P has an all-zero column: initialisation x_i = eps/(n ||P_:,i||) undefined"};
+      finish_csr_packing(c, n);
     } else {
       c->pSing = 1; c->nnzP = n;
     }
     if (needC) {
       copy_csr_checked(c, C, c->csrC, n, "C");
-      c->mC = c->csrC.nrows; c->nnzC = c->csrC.nnz;
-      // empty covering rows make the LP infeasible (0 >= 1), Q17
-      {
-        Seg tmpS = c->csrC;
-        const int64_t before = tmpS.nrows;
-        int64_t saved = c->empty_dropped;
-        compact_rows(c, tmpS);
-        c->empty_cover = (tmpS.nrows != before);
-        c->empty_dropped = saved;
-      }
-      build_plan(c, c->csrC);
-      build_csc(c, c->csrC, n, c->cscC);
-      c->colsumC = dalloc<double>(c, n);
-      c->crecipC = dalloc<double>(c, n);
-      k_col_stats<<<grid_for(c, n), MWU_NT, 0, c->st>>>(n, c->cscC.rowptr, c->cscC.val, nullptr, c->colsumC, c->crecipC);
-      CKL();
+      finish_csr_covering(c, n);
     } else {
       c->cSing = 1; c->nnzC = n;
     }

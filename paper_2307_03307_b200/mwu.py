@@ -68,7 +68,7 @@ EXPORTS = ["mwu_default_options", "mwu_create_csr", "mwu_create_graph", "mwu_sol
            "mwu_get_stats", "mwu_destroy", "mwu_last_error", "mwu_probe_begin", "mwu_step", "mwu_run_probe",
            "mwu_run_iters", "mwu_get_vec", "mwu_vec_len", "mwu_set_record", "mwu_get_structure",
            "mwu_get_scalars", "mwu_get_unique_id", "mwu_profile_iters", "mwu_shard_range",
-           "mwu_simgroup_create", "mwu_simgroup_destroy", "mwu_set_stream"]
+           "mwu_simgroup_create", "mwu_simgroup_destroy", "mwu_set_stream", "mwu_create_gmatch"]
 
 _lib = None
 
@@ -87,6 +87,7 @@ def lib():
         L.mwu_create_csr.argtypes = [ctypes.POINTER(_Csr), ctypes.POINTER(_Csr), ctypes.c_int,
                                      ctypes.POINTER(Options), ctypes.POINTER(vp)]
         L.mwu_create_graph.argtypes = [ctypes.POINTER(_Graph), ctypes.POINTER(Options), ctypes.POINTER(vp)]
+        L.mwu_create_gmatch.argtypes = [ctypes.POINTER(_Graph), vp, vp, ctypes.POINTER(Options), ctypes.POINTER(vp)]
         L.mwu_solve.argtypes = [vp, dbl, i64, ctypes.POINTER(i32)]
         L.mwu_get_x.argtypes = [vp, vp, i64]
         L.mwu_get_stats.argtypes = [vp, ctypes.POINTER(Stats)]
@@ -222,6 +223,21 @@ class Solver:
         ws, rk = dist.get_world_size(), dist.get_rank()
         uid = share_unique_id(get_unique_id)     # world 1 too: the exchange runs through NCCL
         return cls.graph(kind, src, dst, n_vertices, n_left, world=ws, rank=rk, nccl_id=uid, **opts)
+
+    @classmethod
+    def gmatch(cls, src: torch.Tensor, dst: torch.Tensor, n_vertices: int, lb: torch.Tensor, ub: torch.Tensor,
+               **opts) -> "Solver":
+        """Generalized matching l <= M x <= u (mwu_create_gmatch; solve() runs one MIXED probe)."""
+        src = src.to(torch.int32).contiguous()
+        dst = dst.to(torch.int32).contiguous()
+        lb = lb.to(torch.float64).contiguous()
+        ub = ub.to(torch.float64).contiguous()
+        g = _Graph(GRAPH_KINDS["match"], int(n_vertices), int(src.numel()), 0, _ptr(src), _ptr(dst))
+        keep = [src, dst, lb, ub]
+        o = default_options(keep, **opts)
+        h = ctypes.c_void_p()
+        _check(lib().mwu_create_gmatch(ctypes.byref(g), _ptr(lb), _ptr(ub), ctypes.byref(o), ctypes.byref(h)))
+        return cls(h, keep)
 
     @classmethod
     def csr(cls, mode: int, n: int, P=None, C=None, **opts) -> "Solver":
