@@ -45,6 +45,7 @@ typedef int (*fn_commInitRank)(ncclComm_t_*, int, NcclUid, int);
 typedef int (*fn_allReduce)(const void*, void*, size_t, int, int, ncclComm_t_, cudaStream_t);
 typedef int (*fn_allGather)(const void*, void*, size_t, int, ncclComm_t_, cudaStream_t);
 typedef int (*fn_commDestroy)(ncclComm_t_);
+typedef int (*fn_commAbort)(ncclComm_t_);
 typedef const char* (*fn_getErrorString)(int);
 enum { NCCL_FLOAT64_ = 8, NCCL_SUM_ = 0 };
 
@@ -55,6 +56,7 @@ struct NcclLib {
   fn_allReduce allReduce = nullptr;
   fn_allGather allGather = nullptr;
   fn_commDestroy commDestroy = nullptr;
+  fn_commAbort commAbort = nullptr;
   fn_getErrorString errStr = nullptr;
   static NcclLib& get() {
     static NcclLib L;
@@ -69,6 +71,7 @@ struct NcclLib {
       L.allReduce = (fn_allReduce)dlsym(L.h, "ncclAllReduce");
       L.allGather = (fn_allGather)dlsym(L.h, "ncclAllGather");
       L.commDestroy = (fn_commDestroy)dlsym(L.h, "ncclCommDestroy");
+      L.commAbort = (fn_commAbort)dlsym(L.h, "ncclCommAbort");
       L.errStr = (fn_getErrorString)dlsym(L.h, "ncclGetErrorString");
       if (!L.getUniqueId || !L.commInitRank || !L.allReduce || !L.allGather || !L.commDestroy)
         throw std::runtime_error("NCCL library lacks required symbols");
@@ -90,13 +93,24 @@ struct NcclComm : Comm {
     L.check(L.commInitRank(&c, w, id, r), "ncclCommInitRank");
   }
   ~NcclComm() override { if (c) NcclLib::get().commDestroy(c); }
-  void allreduce_sum(double* buf, int64_t n, cudaStream_t st) override {
+  // a failed collective aborts the communicator (pending operations on every rank return
+  // instead of hanging) before the error reaches the caller as MWU_ERR_NCCL
+  void checked(int r, const char* what) {
     NcclLib& L = NcclLib::get();
-    L.check(L.allReduce(buf, buf, (size_t)n, NCCL_FLOAT64_, NCCL_SUM_, c, st), "ncclAllReduce");
+    if (r != 0) {
+      if (L.commAbort && c) { L.commAbort(c); c = nullptr; }
+      L.check(r, what);
+    }
+  }
+  void allreduce_sum(double* buf, int64_t n, cudaStream_t st) override {
+    if (!c) throw std::runtime_error("NCCL communicator aborted by an earlier error");
+    NcclLib& L = NcclLib::get();
+    checked(L.allReduce(buf, buf, (size_t)n, NCCL_FLOAT64_, NCCL_SUM_, c, st), "ncclAllReduce");
   }
   void allgather(const double* in, double* out, int64_t n, cudaStream_t st) override {
+    if (!c) throw std::runtime_error("NCCL communicator aborted by an earlier error");
     NcclLib& L = NcclLib::get();
-    L.check(L.allGather(in, out, (size_t)n, NCCL_FLOAT64_, c, st), "ncclAllGather");
+    checked(L.allGather(in, out, (size_t)n, NCCL_FLOAT64_, c, st), "ncclAllGather");
   }
 };
 

@@ -5,6 +5,8 @@
 #include "storage.cuh"
 #include "comm.cuh"
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: host ranges for nsys / ncu timelines
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -1368,7 +1370,13 @@ void solve(mwu_ctx* c, double eps, int64_t max_iter, int32_t* outcome) {
   CK(cudaEventCreate(&s0)); CK(cudaEventCreate(&s1));
   CK(cudaEventRecord(s0, c->st));
   float loop_ms_total = 0.f;
+  struct Nvtx {                               // one NVTX range per probe (SURVEY §5 tracing)
+    explicit Nvtx(const char* m) { nvtxRangePushA(m); }
+    ~Nvtx() { nvtxRangePop(); }
+  };
+  Nvtx solve_range("mwu_solve");
   auto run_one = [&](double B) -> int {
+    Nvtx probe_range("mwu_probe");
     probe_begin(c, B, eps);
     cudaEvent_t a, b;
     CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
