@@ -38,8 +38,9 @@ NOISE = 2.0 ** -50   # 4 ulps per iteration, as tests/gpu_common.self_drift
 
 @contextlib.contextmanager
 def rounding_noise(seed: int, noise: float = NOISE):
-    """Within this context the oracle's probes inject rounding noise after every update — every
-    element of x, y and z scaled by 1 +- noise with random signs — the size of the differences
+    """Within this context the oracle's probes inject rounding noise every iteration — every
+    element of g and h (before the direction) and, after the update, of x, y and z scaled by
+    1 +- noise with random signs — the size of the differences
     another correct fp64 evaluation (other summation order, a 2-ulp exp) makes per iteration.  A
     full solve that keeps its objective and iteration count under this noise is well conditioned
     (test infrastructure: wraps the oracle's Probe class, no change to its arithmetic)."""
@@ -48,7 +49,15 @@ def rounding_noise(seed: int, noise: float = NOISE):
     base = M.Probe
     rng = np.random.default_rng(seed)
 
+    def perturb(g, h):
+        return (g * (1.0 + noise * rng.choice((-1.0, 1.0), size=g.shape)),
+                h * (1.0 + noise * rng.choice((-1.0, 1.0), size=h.shape)))
+
     class Noisy(base):
+        def __init__(self, *a, **kw):
+            super().__init__(*a, **kw)
+            self.perturb = perturb               # noise through the 1 - g/h cancellation too
+
         def step(self, alpha=None):
             st = super().step(alpha)
             if st == M.RUNNING:
