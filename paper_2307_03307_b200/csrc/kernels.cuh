@@ -214,7 +214,7 @@ __device__ void accept_alpha(Ctl* c, double a, double mx, double mn, double tc, 
   c->sphase = SP_DONE;
   c->sactive = 0;
   if (a < 1.0) { c->status = ST_INFEASIBLE; c->reason = R_ALPHA_LT_1; return; }
-  if (false && c->lazyC && !(tc > 1e-280 && isfinite(tc))) {
+  if (c->lazyC && !(tc > 1e-280 && isfinite(tc))) {
     // lazyC carries S_C of the next iterate from this sum; it underflowed at the old shift, so
     // re-evaluate the accepted alpha with the exact min shift (one extra pass, Q16)
     c->sphase = SP_TCFIX; c->ncand = 1; c->cand[0] = a; c->cea[0] = c->eta * a; c->cexp[0] = 0; c->csq[0] = 0;
@@ -501,10 +501,7 @@ __device__ void finalize(Ctl* c, int action, double* r) {
       if (c->pSing) { c->yS = c->yS + c->alpha * c->dyS; c->sP = c->yS; c->SP = 1.0; }
       else { c->sP = c->newsP; c->SP = r[0]; }
       if (c->cSing) { c->zS = c->zS + c->alpha * c->dzS; c->sC = c->zS; c->SC = 1.0; }
-      else if (c->lazyC) {                   // exact: active records + the inactive aggregate (mzi, Vi)
-        c->sC = c->newsC;
-        c->SC = r[1] + (c->Vi > 0.0 ? c->Vi * exp(-c->eta * (c->mzi - c->newsC)) : 0.0);
-      }
+      else if (c->lazyC) { c->sC = c->newsC; c->SC = c->acc_tc * exp(c->eta * (c->newsC - c->acc_sh)); }
       else { c->sC = c->newsC; c->SC = r[1]; }
       if (!(isfinite(c->SP) && isfinite(c->SC) && c->SP > 0.0 && c->SC > 0.0)) {
         c->nan_flag = 1; c->status = ST_INFEASIBLE;
@@ -1384,23 +1381,10 @@ __global__ void __launch_bounds__(MWU_NT, MWU_SEARCH_MINB) search_pass(SearchArg
 // y += alpha d^(y), z += alpha d^(z) fused with u = exp(eta (y - s_P)),
 // v = exp(-eta (z - s_C)) at the accepted alpha's shifts, and S_P, S_C.
 // has_delta = 0: initial weights only (init) with shifts from A_INIT_EXT.
-// Lazy covering side (fast densest path): the covering rows are updated in the next column kernel,
-// but S_C of the new iterate is summed HERE exactly, over the compacted records of the active rows
-// (z + alpha d^(z), the same z the column kernel will form) with the column kernel's own exp, plus
-// the inactive rows' aggregate — not carried from the search pass, whose candidate sums come from
-// squaring / product chains and are accurate only to ~100 ulps.
-struct LazyRecords {
-  const double *rz, *rdz;
-  const int32_t* cnt;
-  int64_t nstreams, cap;
-  const double* exptab;     // 2^(j/256) (mwu_exp_tab)
-};
-
 __global__ void __launch_bounds__(MWU_NT) update_rows(int64_t mP, double* __restrict__ y, const double* __restrict__ dy,
                                                       double* __restrict__ u, int64_t mC, double* __restrict__ z,
                                                       const double* __restrict__ dz, double* __restrict__ v, Ctl* c,
-                                                      double* part, unsigned int* counter, int has_delta,
-                                                      LazyRecords lr) {
+                                                      double* part, unsigned int* counter, int has_delta) {
   if (c->status != ST_RUNNING) {
     if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(c->h_iter, 0u);
     return;
@@ -1423,18 +1407,6 @@ __global__ void __launch_bounds__(MWU_NT) update_rows(int64_t mP, double* __rest
     const double w = exp(neta * (zi - sC));
     if (v) v[i] = w;
     acc[1] += w;
-  }
-  if (has_delta && lr.rz) {                      // lazy covering side: exact S_C of the new iterate
-    __shared__ double s_tab[256];
-    s_tab[threadIdx.x] = lr.exptab[threadIdx.x];   // MWU_NT == 256
-    __syncthreads();
-    for (int64_t w = blockIdx.x; w < lr.nstreams; w += gridDim.x) {
-      const int64_t n = __ldg(lr.cnt + w), b0 = w * lr.cap;
-      for (int64_t k = threadIdx.x; k < n; k += MWU_NT) {
-        const double zn = __ldcs(lr.rz + b0 + k) + a * __ldcs(lr.rdz + b0 + k);   // as the column kernel forms it
-        acc[1] += mwu_exp_tab(neta * (zn - sC), s_tab);
-      }
-    }
   }
   const int ops[2] = {OP_SUM, OP_SUM};
   reduce_and_finalize<2>(acc, ops, part, counter, c, has_delta ? A_UPDATE : A_INIT_W);

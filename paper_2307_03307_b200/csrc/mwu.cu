@@ -1037,15 +1037,8 @@ void enqueue_update(mwu_ctx* c, cudaStream_t st, int has_delta) {
   // lazyC: the covering side is updated lazily by the next column kernel (only at init are its
   // weight sums formed here, without storing v)
   const int64_t mC = (c->lazyC && has_delta) ? 0 : c->mC;
-  LazyRecords lr{};
-  if (c->lazyC && has_delta) {
-    lr.rz = c->rz; lr.rdz = c->rdz; lr.cnt = c->tcnt; lr.nstreams = c->rec_grid * (MWU_NT / 32);
-    lr.cap = c->rec_cap; lr.exptab = c->exptab;
-  }
-  const int64_t gr = (c->lazyC && has_delta) ? std::max<int64_t>(rows_grid(c, c->mP), std::min<int64_t>(lr.nstreams, c->grid_rows))
-                                             : rows_grid(c, c->mP + mC);
-  update_rows<<<(int)gr, MWU_NT, 0, st>>>(c->mP, c->y, c->dy, c->u, mC, c->z, c->dz, c->v, c->ctl, c->part, c->counter,
-                                         has_delta, lr);
+  update_rows<<<rows_grid(c, c->mP + mC), MWU_NT, 0, st>>>(c->mP, c->y, c->dy, c->u, mC, c->z, c->dz, c->v,
+                                                          c->ctl, c->part, c->counter, has_delta);
   c->launches++;
 }
 
@@ -1133,7 +1126,7 @@ void probe_begin(mwu_ctx* c, double bound, double eps) {
   h.compC = c->compC;
   h.world = c->sharded ? std::max(2, c->world) : 1;   // device: defer partial reductions when sharded
   h.repvars = c->fastC ? 1 : 0;                          // covering kinds: variables replicated
-  h.partupd = (c->sharded && (c->fastC || c->lazyC)) ? 1 : 0;   // their covering rows are local
+  h.partupd = (c->sharded && c->fastC) ? 1 : 0;          // their covering rows are local
   for (int i = 0; i < 32; ++i) h.aguess[i] = c->aguess[i];
   h.status = c->empty_cover ? ST_INFEASIBLE : ST_RUNNING;
   h.reason = c->empty_cover ? R_EMPTY_COVER : R_NONE;
@@ -1588,7 +1581,7 @@ mwu_status mwu_create_graph(const mwu_graph* g, const mwu_options* opt, mwu_ctx*
       memset(&h, 0, sizeof(Ctl));
       h.world = c->sharded ? std::max(2, c->world) : 1;
       h.repvars = c->fastC ? 1 : 0;
-      h.partupd = (c->sharded && (c->fastC || c->lazyC)) ? 1 : 0;
+      h.partupd = (c->sharded && c->fastC) ? 1 : 0;
       CK(cudaMemcpyAsync(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, c->st));
       sync(c);
     }

@@ -166,18 +166,32 @@ NOISE = 2.0 ** -50    # rounding noise injected per iteration: 4 ulps, the typic
                       # reordered sum of a degree-16 row (or a 2-ulp exp) makes
 
 
+def noise_amplitudes(lp: O.LP, noise: float = None):
+    """Relative rounding-noise amplitude per element of the vectors the drift model perturbs: a sum
+    of n terms evaluated in another order (the GPU's atomics / trees against the oracle's CSR-order
+    sums) differs by ~sqrt(n) ulps, so y, z (rows of P, C), g, h (columns of P, C) get
+    NOISE * sqrt(max(1, n)) with n their number of terms, x gets NOISE."""
+    noise = NOISE if noise is None else noise
+    def rows(A):
+        return noise * np.sqrt(np.maximum(1.0, np.diff(A.tocsr().indptr)))
+    def cols(A):
+        return noise * np.sqrt(np.maximum(1.0, np.diff(A.tocsc().indptr)))
+    return {"x": noise, "y": rows(lp.P), "z": rows(lp.C), "g": cols(lp.P), "h": cols(lp.C)}
+
+
 def self_drift(lp: O.LP, eps, alphas, iters, tol_mode="prose"):
     """The ORACLE's own fp64 conditioning along the compared trajectory.  Two reruns inject
     rounding noise of the size another correct fp64 evaluation makes (other summation order, a
-    2-ulp exp): x0 scaled by 1 + s 2^-52; every element of g = P^T w_p and h = C^T w_c scaled by
-    1 + s r NOISE before the direction is formed (so the noise passes through the cancellation in
-    1 - g/h as the GPU's does); and every element of x, y, z scaled likewise after each update
-    (s = +1 / -1 per rerun, r = +-1 at random per element, NOISE = 4 ulps).  drift[t][k] is the
-    largest elementwise relative difference (floor 1e-300) of vector k between the reruns and the
-    reference run after iteration t (t = 0: the initial state).  drift[t]["split"] is True once a
-    rerun accepted a different step size or terminated differently (a decision within the
-    rounding noise of Alg. 3, or of min z >= 1, Q6) or its state drifted beyond
-    SEPARATED: from there the trajectories separate by the method itself."""
+    2-ulp exp): x0 scaled by 1 + s 2^-52; every iteration every element of g = P^T w_p and
+    h = C^T w_c (before the direction, so the noise passes through the 1 - g/h cancellation as the
+    GPU's does) and, after the update, of x, y, z scaled by 1 + s r a_i (s = +1 / -1 per rerun,
+    r = +-1 at random per element, a_i = noise_amplitudes: 4 ulps times sqrt of the element's
+    number of summed terms).  drift[t][k] is the largest elementwise relative difference (floor
+    1e-300) of vector k between the reruns and the reference run after iteration t (t = 0: the
+    initial state).  drift[t]["split"] is True once a rerun accepted a different step size or
+    terminated differently (a decision within the rounding noise of Alg. 3, or of
+    min z >= 1, Q6) or its state drifted beyond SEPARATED: from there the trajectories separate
+    by the method itself."""
     runs = [O.Probe(lp, eps, tol_mode=tol_mode)] + [O.Probe(lp, eps, tol_mode=tol_mode, x0_scale=sc)
                                                     for sc in (1 + 2.0 ** -52, 1 - 2.0 ** -52)]
 
@@ -189,9 +203,10 @@ def self_drift(lp: O.LP, eps, alphas, iters, tol_mode="prose"):
                 r[k] = max(rel_err(_probe_vecs(q)[k], ref[k]) for q in runs[1:])
         return r
     rng = np.random.default_rng(12345)
-    for q, sg in zip(runs[1:], (1.0, -1.0)):      # +-NOISE on every element of g and h, random signs
-        q.perturb = (lambda g, h, sg=sg: (g * (1.0 + sg * NOISE * rng.choice((-1.0, 1.0), size=g.shape)),
-                                          h * (1.0 + sg * NOISE * rng.choice((-1.0, 1.0), size=h.shape))))
+    amp = noise_amplitudes(lp)
+    for q, sg in zip(runs[1:], (1.0, -1.0)):      # noise on every element of g and h, random signs
+        q.perturb = (lambda g, h, sg=sg: (g * (1.0 + sg * amp["g"] * rng.choice((-1.0, 1.0), size=g.shape)),
+                                          h * (1.0 + sg * amp["h"] * rng.choice((-1.0, 1.0), size=h.shape))))
     out = [rec(False)]
     gone = {"split": True, **{k: float("inf") for k in DRIFT_KEYS}}
     for t in range(iters):
@@ -203,8 +218,9 @@ def self_drift(lp: O.LP, eps, alphas, iters, tol_mode="prose"):
             break
         if sts[0] != O.RUNNING:                # all terminated alike: nothing more to compare
             break
-        for q, sg in zip(runs[1:], (1.0, -1.0)):        # elementwise +-NOISE, random signs
-            q.x, q.y, q.z = (v * (1.0 + sg * NOISE * rng.choice((-1.0, 1.0), size=v.shape)) for v in (q.x, q.y, q.z))
+        for q, sg in zip(runs[1:], (1.0, -1.0)):        # elementwise noise, random signs
+            q.x, q.y, q.z = (v * (1.0 + sg * amp[k] * rng.choice((-1.0, 1.0), size=v.shape))
+                             for k, v in (("x", q.x), ("y", q.y), ("z", q.z)))
             q._weights()
         r = rec(False)
         if max(r["x"], r["y"], r["z"]) > SEPARATED:

@@ -29,7 +29,7 @@ WELL_CONDITIONED = {
     "domset-K15,40": ("domset", lambda: gg.complete_bipartite(15, 40)),
     "domset-K20,30+5": ("domset", lambda: gg.plus_random_edges(gg.complete_bipartite(20, 30), 5, 1)),
     "domset-S50+K8,12": ("domset", lambda: gg.disjoint_union(gg.star_graph(50), gg.complete_bipartite(8, 12))),
-    "densest-er400s204": ("densest", lambda: gg.erdos_renyi(400, 1600, seed=204)),
+    "densest-bu310": ("densest", lambda: gg.bipartite_uniform(40, 60, 500, seed=310)),
 }
 
 
@@ -40,29 +40,30 @@ NOISE = 2.0 ** -50   # 4 ulps per iteration, as tests/gpu_common.self_drift
 def rounding_noise(seed: int, noise: float = NOISE):
     """Within this context the oracle's probes inject rounding noise every iteration — every
     element of g and h (before the direction) and, after the update, of x, y and z scaled by
-    1 +- noise with random signs — the size of the differences
+    1 +- a_i with random signs (a_i = gpu_common.noise_amplitudes: noise times sqrt of the number of
+    summed terms) — the size of the differences
     another correct fp64 evaluation (other summation order, a 2-ulp exp) makes per iteration.  A
     full solve that keeps its objective and iteration count under this noise is well conditioned
     (test infrastructure: wraps the oracle's Probe class, no change to its arithmetic)."""
     import numpy as np
     import oracle.mwu_oracle as M
+    from gpu_common import noise_amplitudes
     base = M.Probe
     rng = np.random.default_rng(seed)
-
-    def perturb(g, h):
-        return (g * (1.0 + noise * rng.choice((-1.0, 1.0), size=g.shape)),
-                h * (1.0 + noise * rng.choice((-1.0, 1.0), size=h.shape)))
 
     class Noisy(base):
         def __init__(self, *a, **kw):
             super().__init__(*a, **kw)
-            self.perturb = perturb               # noise through the 1 - g/h cancellation too
+            self.amp = noise_amplitudes(self.lp, noise)
+            amp = self.amp
+            self.perturb = lambda g, h: (g * (1.0 + amp["g"] * rng.choice((-1.0, 1.0), size=g.shape)),
+                                         h * (1.0 + amp["h"] * rng.choice((-1.0, 1.0), size=h.shape)))
 
         def step(self, alpha=None):
             st = super().step(alpha)
             if st == M.RUNNING:
-                self.x, self.y, self.z = (v * (1.0 + noise * rng.choice((-1.0, 1.0), size=v.shape))
-                                          for v in (self.x, self.y, self.z))
+                self.x, self.y, self.z = (v * (1.0 + self.amp[k] * rng.choice((-1.0, 1.0), size=v.shape))
+                                          for k, v in (("x", self.x), ("y", self.y), ("z", self.z)))
                 self._weights()
             return st
     M.Probe = Noisy

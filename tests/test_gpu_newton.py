@@ -56,7 +56,7 @@ def test_standard_step_is_alpha_one(cuda_ok):
         assert S.scalars()["alpha_last"] == 1.0
 
 
-@pytest.mark.parametrize("name", ["bmatch-bu21", "match-er21", "domset-K25,26", "densest-er400s204"])
+@pytest.mark.parametrize("name", ["bmatch-bu21", "match-er21", "domset-K25,26", "densest-bu310"])
 def test_newton_full_solve(cuda_ok, name):
     """Full solve with Newton steps: same optimum as the oracle's Newton solve (1e-6 on these
     well-conditioned instances, iterations printed), Theorem contract on the GPU's x."""

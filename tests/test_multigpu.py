@@ -152,7 +152,7 @@ def test_sharded_fixed_steps_match_oracle(cuda_ok, world, ci):
 
 
 SHARDED_WELL = ["bmatch-bu21", "match-er21", "vcover-K5,200", "domset-K25,26", "domset-K20,30+5",
-                "densest-er400s204"]
+                "densest-bu310"]
 
 
 @pytest.mark.gpu
