@@ -154,10 +154,44 @@ def measured_peak_gbs():
 
 
 # ----------------------------------------------------------------------------- CPU oracle
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class PinnedCore:
+    """Run the oracle pinned to one host core (taskset -c <core> equivalent) and single-threaded
+    BLAS, then restore the affinity: the CPU baseline states exactly the cores it used."""
+
+    def __init__(self, core=0):
+        self.core = core
+
+    def __enter__(self):
+        self.saved = os.sched_getaffinity(0)
+        try:
+            os.sched_setaffinity(0, {self.core})
+        except OSError:
+            pass
+        return self
+
+    def __exit__(self, *a):
+        os.sched_setaffinity(0, self.saved)
+
+
 def cpu_oracle_rate(workload, seed, seconds=15.0, min_iters=3, steps=None):
-    """The oracle as it stands, single process (numpy/scipy, 1 thread of compute), on the
-    same-recipe reduced instance of `workload`; returns iterations/s scaled to the full
-    workload by the nonzero ratio (the per-iteration work is linear in nnz)."""
+    """The oracle as it stands, single process pinned to one core (numpy/scipy, one thread of
+    compute), on the same-recipe reduced instance of `workload`; returns iterations/s scaled to
+    the full workload by the nonzero ratio (the per-iteration work is linear in nnz)."""
+    with PinnedCore(0):
+        return _cpu_oracle_rate(workload, seed, seconds, min_iters, steps)
+
+
+def _cpu_oracle_rate(workload, seed, seconds=15.0, min_iters=3, steps=None):
     import numpy as np  # noqa: F401
 
     import graphgen as gg
@@ -228,7 +262,8 @@ def run_reference(args):
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": f"{args.workload}: {desc}", "kind": kind, "eps": eps},
-        "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": 1, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model(), "pinned_core": 0, "host_cores": os.cpu_count()},
         "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     del cpu_it
@@ -358,7 +393,8 @@ def run_ours(args):
         rate, nnz_s, it, el, sample = cpu_oracle_rate(args.workload, args.seed, seconds=args.cpu_seconds)
         cpu = {"value": rate * nnz_s / nnz_iter, "unit": "iterations/s", "cores": 1, "kind": "oracle",
                "sample": sample + f"; rate scaled to the full workload by nnz ({nnz_s:,} -> {nnz_iter:,})",
-               "nnz_per_s": rate * nnz_s}
+               "nnz_per_s": rate * nnz_s, "cpu_model": cpu_model(), "pinned_core": 0,
+               "host_cores": os.cpu_count()}
     # e2e: the public API from pinned host buffers: create (H2D of the edge list) + K steps +
     # D2H of x_out, device-timed
     e2e = None

@@ -1514,6 +1514,9 @@ __device__ __forceinline__ bool act_bit(const uint32_t* act, int e) { return (__
 #ifndef MWU_COL_MINB
 #define MWU_COL_MINB 2        // resident column CTAs per SM (grid = MWU_COL_MINB x SMs)
 #endif
+#ifndef MWU_COL_XALL
+#define MWU_COL_XALL 0        // 1: load x of every edge at the tile start (no dependent load later)
+#endif
 #ifndef MWU_COL_STAGES
 #define MWU_COL_STAGES 4
 #endif
@@ -1614,7 +1617,12 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
       const int j = k * MWU_NT + threadIdx.x;
       pw[k] = j < rows ? sac[j >> 5] : 0u;
       had[k] = (pw[k] >> lane) & 1u;
+#if MWU_COL_XALL
+      if (j < rows) xe[k] = x2[e0 + j];                         // x of every edge, early
+      if (had[k]) dp[k] = d2[e0 + j];
+#else
       if (had[k]) { xe[k] = x2[e0 + j]; dp[k] = d2[e0 + j]; }
+#endif
     }
 #pragma unroll
     for (int k = 0; k < kColEdges; ++k) {
@@ -1640,7 +1648,7 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
         if (gdbg) { gdbg[2 * e] = g0; gdbg[2 * e + 1] = g1; hdbg[2 * e] = h; hdbg[2 * e + 1] = h; }
         // g >= h gives fl(g/h) >= 1, i.e. d = 0 exactly
         const bool a0 = g0 < h, a1 = g1 < h;
-        if ((a0 || a1) && !had[k]) xe[k] = x2[e];   // newly active: fetch x
+        if (!MWU_COL_XALL && (a0 || a1) && !had[k]) xe[k] = x2[e];   // newly active: fetch x
         if (a0) d0 = mwu_direction(g0, h, xe[k].x, sigma);
         if (a1) d1 = mwu_direction(g1, h, xe[k].y, sigma);
       }
