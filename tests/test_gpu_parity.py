@@ -432,3 +432,25 @@ def test_compact_covering_rows_parity(cuda_ok, kind, compc):
         probe = O.Probe(lp, EPS[kind], max_iter=5000)
         S = solver_for(kind, G, compact_cover=compc)
         lockstep(S, probe, B, EPS[kind], 50, alphas=None, drift=self_drift(lp, EPS[kind], None, 50))
+
+
+def test_inputs_produced_on_a_side_stream(cuda_ok):
+    """mwu_options.stream: the edge list is produced asynchronously on a torch side stream behind a
+    long sleep kernel; create (called with that stream current) must wait for it — the structure
+    equals the one built from the finished list — and the output copy lands on that stream too."""
+    from paper_2307_03307_b200 import Solver
+    G = gg.rmat(12, 16, seed=9)
+    ref = solver_for("vcover", G).structure("degree")
+    side = torch.cuda.Stream()
+    src_h, dst_h = G.src.pin_memory(), G.dst.pin_memory()
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(200_000_000)                       # ~0.1 s of GPU time before the copies
+        src = src_h.to("cuda", non_blocking=True)
+        dst = dst_h.to("cuda", non_blocking=True)
+        S = Solver.graph("vcover", src, dst, G.n_vertices)  # options.stream = side
+        deg = S.structure("degree")
+        S.solve(0.05, 200)
+        x = S.x()
+    side.synchronize()
+    assert torch.equal(deg, ref)
+    assert x.abs().sum().item() > 0

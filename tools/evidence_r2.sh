@@ -18,7 +18,12 @@ done
 for spec in "c4 col_densest_fast|search_pass 40" "c5 col_match_fast|search_pass 30" "c2 vc_scatter|edge_sum_compact|search_pass|col_vertex 60" "c3 csr_scatter|edge_sum_compact|search_pass|col_vertex 60"; do
   set -- $spec
   timeout 300 python tools/diag.py --workload $1 --iters 12 --active 0 > gpurun_out/diag_$1.log 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$2" -s $3 -c 4 \
-      -o gpurun_out/prof_r2_$1 python tools/diag.py --workload $1 --iters 12 --active 0 > gpurun_out/ncu_full_$1.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$2" -s $3 -c 3 \
+      -o /tmp/prof_r2_$1 python tools/diag.py --workload $1 --iters 12 --active 0 > gpurun_out/ncu_full_$1.log 2>&1
+  # keep the summaries only (gpurun brings back <= 64 MiB): raw metrics and per-line CUDA source stalls
+  ncu -i /tmp/prof_r2_$1.ncu-rep --page raw --csv > gpurun_out/prof_r2_$1_raw.csv 2>/dev/null
+  ncu -i /tmp/prof_r2_$1.ncu-rep --page source --csv --print-source cuda,sass --launch-count 1 2>/dev/null | gzip > gpurun_out/prof_r2_$1_src.csv.gz
+  rm -f /tmp/prof_r2_$1.ncu-rep
 done
+du -sh gpurun_out
 echo done

@@ -80,11 +80,12 @@ keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
         "launch__registers_per_thread", "smsp__inst_executed.sum"]
 for w in ("c4", "c5", "c2", "c3"):
-    rep = os.path.join(G, f"prof_r2_{w}.ncu-rep")
-    if not os.path.exists(rep):
+    rawp = os.path.join(G, f"prof_r2_{w}_raw.csv")
+    if not os.path.exists(rawp):
         continue
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rr = list(csv.reader(raw.splitlines()))
+    rr = list(csv.reader(open(rawp)))
+    if not rr:
+        continue
     hh = rr[0]
     lines = [f"ncu --set full --clock-control none --import-source on (tools/evidence_r2.sh) python tools/diag.py "
              f"--workload {w} --iters 12 --active 0   ({w}, first probe, iterations ~10; round 2, {tag})", ""]
