@@ -326,12 +326,21 @@ def run_ours(args):
         state["probes"] += 1
         S.probe_begin(state["B"], eps)
 
-    def run_steps(k):
+    window = {"phase_ms": {p: 0.0 for p in ("column", "step", "search", "update")}, "passes": 0.0}
+
+    def run_steps(k, account=False):
         done = 0
         while done < k:
-            t_before = S.scalars()["t"]
+            sc0 = S.scalars()
+            ph0 = S.stats()["t_phase_ms"]
             out = S.run_iters(k - done)
-            done += int(S.scalars()["t"] - t_before)
+            sc1 = S.scalars()
+            done += int(sc1["t"] - sc0["t"])
+            if account:        # device-side phase times (%globaltimer, inside the graph) of these steps
+                ph1 = S.stats()["t_phase_ms"]
+                for p in window["phase_ms"]:
+                    window["phase_ms"][p] += ph1[p] - ph0[p]
+                window["passes"] += sc1["passes"] - sc0["passes"]
             if out != "running":
                 next_probe(out)
         return done
@@ -344,7 +353,7 @@ def run_ours(args):
     launches0 = None
     with Clocks(lr) as clk:
         e0.record()
-        n_done = run_steps(args.steps)
+        n_done = run_steps(args.steps, account=True)
         e1.record()
         torch.cuda.synchronize()
     if ws > 1:
@@ -446,6 +455,11 @@ def run_ours(args):
                      "traffic_source": (ncu_traffic(args.workload, dom)[1] or {}).get("source"),
                      "peak_source": peak_kind},
         "phases": phases, "search_passes_per_iter": passes_per_iter,
+        "timed_window": {"phase_ms_per_iter": {p: v / max(1, n_done) for p, v in window["phase_ms"].items()},
+                         "search_passes_per_iter": window["passes"] / max(1, n_done),
+                         "note": "device-side phase times of the timed graph-launched iterations (%globaltimer at "
+                                 "each phase end, launch gaps included); `phases` is a host-driven profile of the "
+                                 "iterations after the window"},
         "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": int(round(launches_per_iter * n_done)),
         "clocks": clk.summary(),

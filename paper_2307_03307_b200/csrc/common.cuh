@@ -260,8 +260,12 @@ __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
+#ifndef MWU_SCH
 #define MWU_SCH 512    // rows per streamed chunk
+#endif
+#ifndef MWU_SST
 #define MWU_SST 4      // pipeline stages
+#endif
 
 // Stream rows [0, n) of three fp64 arrays through shared memory in chunks of MWU_SCH, chunk k
 // of the grid-stride sequence going to stage (it % MWU_SST); calls f(a, b, c, i) once per row.

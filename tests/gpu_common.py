@@ -162,8 +162,8 @@ def _probe_vecs(p: O.Probe):
 
 
 SEPARATED = 1e-3      # state drift beyond which two fp64 trajectories are no longer comparable
-NOISE = 2.0 ** -50    # rounding noise injected per iteration: 4 ulps, the typical difference a
-                      # reordered sum of a degree-16 row (or a 2-ulp exp) makes
+NOISE = 2.0 ** -49    # rounding noise per iteration and per summed term: 8 ulps (a 2-ulp exp, a
+                      # product, the shift and its reordered sums; times sqrt(#terms))
 
 
 def noise_amplitudes(lp: O.LP, noise: float = None):
@@ -185,7 +185,7 @@ def self_drift(lp: O.LP, eps, alphas, iters, tol_mode="prose"):
     2-ulp exp): x0 scaled by 1 + s 2^-52; every iteration every element of g = P^T w_p and
     h = C^T w_c (before the direction, so the noise passes through the 1 - g/h cancellation as the
     GPU's does) and, after the update, of x, y, z scaled by 1 + s r a_i (s = +1 / -1 per rerun,
-    r = +-1 at random per element, a_i = noise_amplitudes: 4 ulps times sqrt of the element's
+    r = +-1 at random per element, a_i = noise_amplitudes: 8 ulps times sqrt of the element's
     number of summed terms).  drift[t][k] is the largest elementwise relative difference (floor
     1e-300) of vector k between the reruns and the reference run after iteration t (t = 0: the
     initial state).  drift[t]["split"] is True once a rerun accepted a different step size or

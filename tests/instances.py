@@ -33,7 +33,7 @@ WELL_CONDITIONED = {
 }
 
 
-NOISE = 2.0 ** -50   # 4 ulps per iteration, as tests/gpu_common.self_drift
+NOISE = 2.0 ** -49   # 8 ulps per iteration and summed term, as tests/gpu_common.self_drift
 
 
 @contextlib.contextmanager

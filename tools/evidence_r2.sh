@@ -12,7 +12,7 @@ timeout 1500 python bench.py --workload c5 --steps 10 --warmup 3 --no-cpu --no-e
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 for w in c4 c2 c3 c5; do
   timeout 600 python bench.py --workload $w --steps 4 --warmup 3 --no-cpu --no-e2e --no-solve --profile-iters 3 > gpurun_out/plain_$w.log 2>&1 && \
-  timeout 900 ncu --metrics $M --clock-control none -c 300 --csv --log-file gpurun_out/launches_$w.csv \
+  timeout 900 ncu --metrics $M --clock-control none -k regex:"col_|search_pass|update_rows|dy_finalize|edge_sum|csr_scatter|vc_scatter|inactive|step_done" -c 200 --csv --log-file gpurun_out/launches_$w.csv \
       python bench.py --workload $w --steps 4 --warmup 3 --no-cpu --no-e2e --no-solve --profile-iters 3 > gpurun_out/ncu_launch_$w.log 2>&1
 done
 for spec in "c4 col_densest_fast|search_pass 40" "c5 col_match_fast|search_pass 30" "c2 vc_scatter|edge_sum_compact|search_pass|col_vertex 60" "c3 csr_scatter|edge_sum_compact|search_pass|col_vertex 60"; do
