@@ -261,10 +261,10 @@ __device__ __forceinline__ void fence_barrier_init() {
 }
 
 #ifndef MWU_SCH
-#define MWU_SCH 512    // rows per streamed chunk
+#define MWU_SCH 1024   // rows per streamed chunk (search: 1024 x 3 stages measured 7% faster than 512 x 4)
 #endif
 #ifndef MWU_SST
-#define MWU_SST 4      // pipeline stages
+#define MWU_SST 3      // pipeline stages
 #endif
 
 // Stream rows [0, n) of three fp64 arrays through shared memory in chunks of MWU_SCH, chunk k

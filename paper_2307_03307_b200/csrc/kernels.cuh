@@ -1514,9 +1514,6 @@ __device__ __forceinline__ bool act_bit(const uint32_t* act, int e) { return (__
 #ifndef MWU_COL_MINB
 #define MWU_COL_MINB 2        // resident column CTAs per SM (grid = MWU_COL_MINB x SMs)
 #endif
-#ifndef MWU_COL_XALL
-#define MWU_COL_XALL 0        // 1: load x of every edge at the tile start (no dependent load later)
-#endif
 #ifndef MWU_COL_STAGES
 #define MWU_COL_STAGES 4
 #endif
@@ -1617,12 +1614,11 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
       const int j = k * MWU_NT + threadIdx.x;
       pw[k] = j < rows ? sac[j >> 5] : 0u;
       had[k] = (pw[k] >> lane) & 1u;
-#if MWU_COL_XALL
-      if (j < rows) xe[k] = x2[e0 + j];                         // x of every edge, early
+      // x of EVERY edge, issued at the tile start: an edge that turns active needs it for its
+      // direction, and a load issued only then stalls the warp (measured: column 4.03 -> 3.73 ms
+      // on c4 despite the extra reads of edges that stay inactive)
+      if (j < rows) xe[k] = x2[e0 + j];
       if (had[k]) dp[k] = d2[e0 + j];
-#else
-      if (had[k]) { xe[k] = x2[e0 + j]; dp[k] = d2[e0 + j]; }
-#endif
     }
 #pragma unroll
     for (int k = 0; k < kColEdges; ++k) {
@@ -1648,7 +1644,6 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
         if (gdbg) { gdbg[2 * e] = g0; gdbg[2 * e + 1] = g1; hdbg[2 * e] = h; hdbg[2 * e + 1] = h; }
         // g >= h gives fl(g/h) >= 1, i.e. d = 0 exactly
         const bool a0 = g0 < h, a1 = g1 < h;
-        if (!MWU_COL_XALL && (a0 || a1) && !had[k]) xe[k] = x2[e];   // newly active: fetch x
         if (a0) d0 = mwu_direction(g0, h, xe[k].x, sigma);
         if (a1) d1 = mwu_direction(g1, h, xe[k].y, sigma);
       }
@@ -1706,7 +1701,7 @@ __global__ void __launch_bounds__(MWU_NT, MWU_MATCH_MINB) col_match_fast(int64_t
                                                          const double* __restrict__ u, double* __restrict__ x,
                                                          double* __restrict__ d, double* __restrict__ dy,
                                                          double* gdbg, double* hdbg, Ctl* c, double* part,
-                                                         unsigned int* counter) {
+                                                         unsigned int* counter, uint32_t* __restrict__ act) {
   if (c->status != ST_RUNNING) return;
   const double rSP = 1.0 / c->SP, invB = c->invB, sigma = c->sigma, ap = c->alpha_prev;
   const int apply = c->apply_prev;
@@ -1717,11 +1712,17 @@ __global__ void __launch_bounds__(MWU_NT, MWU_MATCH_MINB) col_match_fast(int64_t
   for (int64_t base = (int64_t)blockIdx.x * chunk; base < E; base += (int64_t)gridDim.x * chunk) {
     double xe[U], dp[U], us[U], ud[U];
     int sr[U], dr[U];
+    uint32_t pw[U];                // activity word of the warp's 32 edges: bit = d > 0 in the last step
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const int64_t e = base + k * MWU_NT + threadIdx.x;
-      if (e < E) { xe[k] = x[e]; dp[k] = d[e]; sr[k] = __ldg(srow + e); dr[k] = __ldg(drow + e); }
-      else { sr[k] = -1; dr[k] = -1; }
+      pw[k] = 0u;
+      dp[k] = 0.0;
+      if (e < E) {
+        pw[k] = __ldg(act + (e >> 5));
+        if ((pw[k] >> lane) & 1u) { xe[k] = x[e]; dp[k] = d[e]; }   // x, d only of the previously active
+        sr[k] = __ldg(srow + e); dr[k] = __ldg(drow + e);
+      } else { sr[k] = -1; dr[k] = -1; }
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
@@ -1731,16 +1732,24 @@ __global__ void __launch_bounds__(MWU_NT, MWU_MATCH_MINB) col_match_fast(int64_t
     for (int k = 0; k < U; ++k) {
       const int64_t e = base + k * MWU_NT + threadIdx.x;
       double de = 0.0;
+      const bool had = (pw[k] >> lane) & 1u;
       if (e < E) {
-        if (apply && dp[k] != 0.0) { xe[k] = xe[k] + ap * dp[k]; x[e] = xe[k]; }   // P:677 (lazy)
+        if (apply && had) { xe[k] = xe[k] + ap * dp[k]; x[e] = xe[k]; }            // P:677 (lazy)
         const double g = us[k] * rSP + ud[k] * rSP;                                // M^T w_p
-        if (g < invB) de = mwu_direction(g, invB, xe[k], sigma);                   // g >= h: d = 0
-        if (de != dp[k]) d[e] = de;
+        if (g < invB) {                                                            // g >= h: d = 0
+          if (!had) xe[k] = x[e];                                                  // newly active: x
+          de = mwu_direction(g, invB, xe[k], sigma);
+        }
+        if (de > 0.0 && de != dp[k]) d[e] = de;                                    // zeros live in `act`
         if (gdbg) { gdbg[e] = g; hdbg[e] = invB; }
         acc[0] = fmax(acc[0], de);
         acc[1] += invB * de;
       }
       const bool want = de > 0.0;
+      {
+        const uint32_t bw = __ballot_sync(0xffffffffu, want);
+        if (lane == 0 && e < E && bw != pw[k]) act[e >> 5] = bw;
+      }
       if (want) red_add_f64(dy + dr[k], de);                      // dst side
       if (__any_sync(0xffffffffu, want)) {                        // src side: sorted runs
         double run;
@@ -1950,6 +1959,21 @@ __global__ void flush_pairs(int64_t E, double* __restrict__ x, const double* __r
 
 // Vector hooks of the fast densest path: d (zeros where the activity bit is clear) and
 // d^(z)_e = d_2e + d_2e+1 (W d), regardless of the probe status.
+__global__ void d_from_act1(int64_t E, const double* __restrict__ d, const uint32_t* __restrict__ act,
+                            double* __restrict__ dout) {     // one variable per edge (matching)
+  for (int64_t e = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; e < E; e += (int64_t)gridDim.x * MWU_NT)
+    dout[e] = act_bit(act, (int)e) ? d[e] : 0.0;
+}
+
+// x += alpha_prev d where the activity bit is set (end of probe / hooks), one variable per edge
+__global__ void flush_act1(int64_t E, double* __restrict__ x, const double* __restrict__ d,
+                           const uint32_t* __restrict__ act, const Ctl* c) {
+  if (!c->apply_prev) return;
+  const double a = c->alpha_prev;
+  for (int64_t e = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; e < E; e += (int64_t)gridDim.x * MWU_NT)
+    if (act_bit(act, (int)e)) x[e] = x[e] + a * d[e];
+}
+
 __global__ void d_from_act(int64_t E, const double* __restrict__ d, const uint32_t* __restrict__ act,
                            double* __restrict__ dout, double* __restrict__ dzout) {
   const double2* d2 = reinterpret_cast<const double2*>(d);

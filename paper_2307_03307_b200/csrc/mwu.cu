@@ -302,6 +302,10 @@ void alloc_vectors(mwu_ctx* c) {
     c->rv = dalloc<double>(c, nrec);
     c->tcnt = dalloc<int32_t>(c, c->rec_grid * (MWU_NT / 32));
   }
+  if (c->kind == K_MATCH && c->scatterP) {   // matching fast path: activity bits of d
+    c->act = dalloc<uint32_t>(c, (c->E + 31) / 32 + 1);
+    CK(cudaMemsetAsync(c->act, 0, ((c->E + 31) / 32 + 1) * sizeof(uint32_t), c->st));
+  }
   if (c->lazyC) {
     c->act = dalloc<uint32_t>(c, c->ntilesC * (MWU_CT / 32));
     CK(cudaMemsetAsync(c->act, 0, c->ntilesC * (MWU_CT / 32) * sizeof(uint32_t), c->st));
@@ -866,7 +870,7 @@ void enqueue_column(mwu_ctx* c, cudaStream_t st) {
         const int g = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, MWU_MATCH_MINB * c->sms));
         col_match_fast<<<g, MWU_NT, 0, st>>>(c->E, c->srow, c->drow, c->u, c->x, c->d, c->dy,
                                             c->record ? c->gdbg : nullptr, c->record ? c->hdbg : nullptr,
-                                            c->ctl, c->part, c->counter);
+                                            c->ctl, c->part, c->counter, c->act);
         c->launches++;
         break;
       }
@@ -1136,6 +1140,7 @@ void probe_begin(mwu_ctx* c, double bound, double eps) {
   h.h_search = 0;
   CK(cudaMemcpyAsync(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, c->st));
   if (c->lazyC) CK(cudaMemsetAsync(c->act, 0, c->ntilesC * (MWU_CT / 32) * sizeof(uint32_t), c->st));
+  else if (c->act) CK(cudaMemsetAsync(c->act, 0, ((c->E + 31) / 32 + 1) * sizeof(uint32_t), c->st));
   // x_i = eps / (n ||P_{:,i}||_inf)
   double cm = 1.0;
   const double* colmax = nullptr;
@@ -1277,6 +1282,7 @@ void profile_iters(mwu_ctx* c, int64_t k, double* out) {
 
 void flush(mwu_ctx* c) {
   if (c->lazyC) flush_pairs<<<rows_grid(c, c->E), MWU_NT, 0, c->st>>>(c->E, c->x, c->d, c->z, c->act, c->ctl);
+  else if (c->act) flush_act1<<<rows_grid(c, c->E), MWU_NT, 0, c->st>>>(c->E, c->x, c->d, c->act, c->ctl);
   else flush_x<<<rows_grid(c, c->n), MWU_NT, 0, c->st>>>(c->n, c->x, c->d, c->ctl);
   CKL();
   int zero = 0;
@@ -1807,6 +1813,10 @@ mwu_status mwu_get_vec(mwu_ctx* c, int which, double* out, int64_t len) {
       case MWU_VEC_D:
         if (c->lazyC) {
           d_from_act<<<rows_grid(c, c->E), MWU_NT, 0, c->st>>>(c->E, c->d, c->act, c->tmp, nullptr);
+          CKL();
+          src = c->tmp;
+        } else if (c->act) {
+          d_from_act1<<<rows_grid(c, c->E), MWU_NT, 0, c->st>>>(c->E, c->d, c->act, c->tmp);
           CKL();
           src = c->tmp;
         } else src = c->d;

@@ -37,8 +37,9 @@ for w in ("c4", "c2", "c3", "c5"):
     ik, im, iv, iid = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
     per = collections.defaultdict(dict)
     for r in rows[1:]:
-        if "mwu::" in r[ik][:12]:
-            per[(r[iid], r[ik].split("(")[0])][r[im]] = float(r[iv].replace(",", ""))
+        name = r[ik].split("(")[0].replace("void ", "").replace("mwu::", "")
+        if name in PHASE_OF or name.startswith(("col_", "search", "update", "dy_", "edge_", "csr_", "vc_", "inactive")):
+            per[(r[iid], "mwu::" + name)][r[im]] = float(r[iv].replace(",", ""))
     agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0])
     for (i, k), m in per.items():
         a = agg[k]
