@@ -1690,72 +1690,136 @@ __global__ void __launch_bounds__(MWU_NT, MWU_COL_MINB) col_densest_fast(
 // g_e = w_p[r(src)] + w_p[r(dst)] (M^T), d_e, and the forward product
 // d^(y) = M d scattered into the vertex vector (src side: warp-segmented runs of the sorted edge
 // list; dst side: one fp64 reduction per nonzero d_e).  Reduces max d and sum(d)/M.
-#ifndef MWU_MATCH_MINB
-#define MWU_MATCH_MINB 3
+// Fed like the c4 kernel: each 1024-edge tile's stream (src / dst rows, activity words) is
+// staged in shared memory by the bulk-copy engine kColStages tiles ahead, and the u gathers of
+// tile i+1 are in flight while tile i is computed, so every thread keeps 2 kColEdges random
+// gathers outstanding (the kernel is bound by the latency of the random destination-side
+// gathers; c5 column 24.3 -> 20.4 ms against a grid-stride loop).
+constexpr int kMOffD = MWU_CT * 4, kMOffA = kMOffD + MWU_CT * 4;
+constexpr int kMStageBytes = ((kMOffA + (MWU_CT / 32) * 4) + 127) / 128 * 128;
+constexpr size_t kMSmem = (size_t)kColStages * kMStageBytes;
+#ifndef MWU_MT_MINB
+#define MWU_MT_MINB 2
 #endif
-#ifndef MWU_MATCH_U
-#define MWU_MATCH_U 2         // edges per thread per grid-stride step
-#endif
-__global__ void __launch_bounds__(MWU_NT, MWU_MATCH_MINB) col_match_fast(int64_t E, const int32_t* __restrict__ srow,
-                                                         const int32_t* __restrict__ drow,
-                                                         const double* __restrict__ u, double* __restrict__ x,
-                                                         double* __restrict__ d, double* __restrict__ dy,
-                                                         double* gdbg, double* hdbg, Ctl* c, double* part,
-                                                         unsigned int* counter, uint32_t* __restrict__ act) {
+
+__device__ __forceinline__ void mt_issue(char* stage, uint64_t* bar, int tile, int64_t E, const int32_t* srow,
+                                         const int32_t* drow, const uint32_t* act) {
+  const int64_t e0 = (int64_t)tile * MWU_CT;
+  const int rows = (int)min((int64_t)MWU_CT, E - e0);
+  const uint32_t bi = r16(rows * 4u), ba = r16(((rows + 31) / 32) * 4u);
+  mbar_expect_tx(bar, 2 * bi + ba);
+  const uint64_t pf = pol_first();
+  tma_load_1d_hint(stage, srow + e0, bi, bar, pf);
+  tma_load_1d_hint(stage + kMOffD, drow + e0, bi, bar, pf);
+  tma_load_1d_hint(stage + kMOffA, act + (e0 >> 5), ba, bar, pf);
+}
+
+__device__ __forceinline__ void mt_gather(const char* stage, int rows, const double* __restrict__ u, double* us,
+                                          double* ud) {
+  const int32_t* ssr = reinterpret_cast<const int32_t*>(stage);
+  const int32_t* sdr = reinterpret_cast<const int32_t*>(stage + kMOffD);
+#pragma unroll
+  for (int k = 0; k < kColEdges; ++k) {
+    const int j = k * MWU_NT + threadIdx.x;
+    if (j < rows) { us[k] = __ldg(u + ssr[j]); ud[k] = __ldg(u + sdr[j]); }
+  }
+}
+
+__global__ void __launch_bounds__(MWU_NT, MWU_MT_MINB) col_match_fast(
+    int64_t E64, const int32_t* __restrict__ srow, const int32_t* __restrict__ drow, const double* __restrict__ u,
+    double* __restrict__ x, double* __restrict__ d, double* __restrict__ dy, double* gdbg, double* hdbg, Ctl* c,
+    double* part, unsigned int* counter, uint32_t* __restrict__ act) {
   if (c->status != ST_RUNNING) return;
   const double rSP = 1.0 / c->SP, invB = c->invB, sigma = c->sigma, ap = c->alpha_prev;
   const int apply = c->apply_prev;
   const int lane = threadIdx.x & 31;
+  const int64_t E = E64;
   double acc[2] = {-INFINITY, 0.0};
-  constexpr int U = MWU_MATCH_U;
-  const int64_t chunk = (int64_t)U * MWU_NT;
-  for (int64_t base = (int64_t)blockIdx.x * chunk; base < E; base += (int64_t)gridDim.x * chunk) {
-    double xe[U], dp[U], us[U], ud[U];
-    int sr[U], dr[U];
-    uint32_t pw[U];                // activity word of the warp's 32 edges: bit = d > 0 in the last step
+  extern __shared__ __align__(128) char csm[];
+  __shared__ __align__(8) uint64_t full[kColStages], empty[kColStages];
+  const int ntiles = (int)((E + MWU_CT - 1) / MWU_CT);
+  const int mine = (ntiles > (int)blockIdx.x) ? (ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kColStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], MWU_NT / 32); }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int k = 0; k < mine && k < kColStages; ++k)
+      mt_issue(csm + k * kMStageBytes, &full[k], blockIdx.x + k * gridDim.x, E, srow, drow, act);
+  double us[kColEdges], ud[kColEdges], nus[kColEdges], nud[kColEdges];
+  if (mine > 0) {
+    mbar_wait(&full[0], 0u);
+    mt_gather(csm, (int)min((int64_t)MWU_CT, E - (int64_t)blockIdx.x * MWU_CT), u, us, ud);
+  }
+  auto body = [&](int kt, double (&us)[kColEdges], double (&ud)[kColEdges], double (&nus)[kColEdges],
+                  double (&nud)[kColEdges]) {
+    const int tile = blockIdx.x + kt * gridDim.x;
+    const int slot = kt % kColStages;
+    char* stg = csm + slot * kMStageBytes;
+    const int64_t e0 = (int64_t)tile * MWU_CT;
+    const int rows = (int)min((int64_t)MWU_CT, E - e0);
+    if (kt + 1 < mine) {
+      const int ns = (kt + 1) % kColStages;
+      mbar_wait(&full[ns], (uint32_t)(((kt + 1) / kColStages) & 1));
+      const int nrows = (int)min((int64_t)MWU_CT, E - (int64_t)(tile + (int)gridDim.x) * MWU_CT);
+      mt_gather(csm + ns * kMStageBytes, nrows, u, nus, nud);
+    }
+    const int32_t* ssr = reinterpret_cast<const int32_t*>(stg);
+    const int32_t* sdr = reinterpret_cast<const int32_t*>(stg + kMOffD);
+    const uint32_t* sac = reinterpret_cast<const uint32_t*>(stg + kMOffA);
+    double xe[kColEdges], dp[kColEdges];
+    uint32_t pw[kColEdges];
 #pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t e = base + k * MWU_NT + threadIdx.x;
-      pw[k] = 0u;
+    for (int k = 0; k < kColEdges; ++k) {                        // x, d of the previously active
+      const int j = k * MWU_NT + threadIdx.x;
+      pw[k] = j < rows ? sac[j >> 5] : 0u;
       dp[k] = 0.0;
-      if (e < E) {
-        pw[k] = __ldg(act + (e >> 5));
-        if ((pw[k] >> lane) & 1u) { xe[k] = x[e]; dp[k] = d[e]; }   // x, d only of the previously active
-        sr[k] = __ldg(srow + e); dr[k] = __ldg(drow + e);
-      } else { sr[k] = -1; dr[k] = -1; }
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      if (sr[k] >= 0) { us[k] = __ldg(u + sr[k]); ud[k] = __ldg(u + dr[k]); }
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t e = base + k * MWU_NT + threadIdx.x;
-      double de = 0.0;
       const bool had = (pw[k] >> lane) & 1u;
-      if (e < E) {
-        if (apply && had) { xe[k] = xe[k] + ap * dp[k]; x[e] = xe[k]; }            // P:677 (lazy)
-        const double g = us[k] * rSP + ud[k] * rSP;                                // M^T w_p
-        if (g < invB) {                                                            // g >= h: d = 0
-          if (!had) xe[k] = x[e];                                                  // newly active: x
+      // x of EVERY edge, issued at the tile start (an edge that turns active needs it for its
+      // direction; a load issued only then stalls the warp: c5 column 22.7 -> 20.4 ms)
+      if (j < rows) xe[k] = x[e0 + j];
+      if (had) dp[k] = d[e0 + j];
+    }
+#pragma unroll
+    for (int k = 0; k < kColEdges; ++k) {
+      const int j = k * MWU_NT + threadIdx.x;
+      const int64_t e = e0 + j;
+      const bool valid = j < rows;
+      const int sr = valid ? ssr[j] : -1, dr = valid ? sdr[j] : -1;
+      const bool had = (pw[k] >> lane) & 1u;
+      double de = 0.0;
+      if (valid) {
+        if (apply && had) { xe[k] = xe[k] + ap * dp[k]; x[e] = xe[k]; }             // P:677 (lazy)
+        const double g = us[k] * rSP + ud[k] * rSP;                                 // M^T w_p
+        if (g < invB) {                                                             // g >= h: d = 0
           de = mwu_direction(g, invB, xe[k], sigma);
         }
-        if (de > 0.0 && de != dp[k]) d[e] = de;                                    // zeros live in `act`
+        if (de > 0.0 && de != dp[k]) d[e] = de;                                     // zeros live in `act`
         if (gdbg) { gdbg[e] = g; hdbg[e] = invB; }
         acc[0] = fmax(acc[0], de);
         acc[1] += invB * de;
       }
       const bool want = de > 0.0;
-      {
-        const uint32_t bw = __ballot_sync(0xffffffffu, want);
-        if (lane == 0 && e < E && bw != pw[k]) act[e >> 5] = bw;
-      }
-      if (want) red_add_f64(dy + dr[k], de);                      // dst side
+      const uint32_t bw = __ballot_sync(0xffffffffu, want);
+      if (lane == 0 && valid && bw != pw[k]) act[e >> 5] = bw;
+      if (want) red_add_f64(dy + dr, de);                         // dst side
       if (__any_sync(0xffffffffu, want)) {                        // src side: sorted runs
         double run;
-        if (warp_run_sum(sr[k], de, run) && run > 0.0) red_add_f64(dy + sr[k], run);
+        if (warp_run_sum(sr, de, run) && run > 0.0) red_add_f64(dy + sr, run);
       }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+    if (threadIdx.x == 0 && kt + kColStages < mine) {
+      mbar_wait(&empty[slot], (uint32_t)((kt / kColStages) & 1));
+      mt_issue(stg, &full[slot], blockIdx.x + (kt + kColStages) * gridDim.x, E, srow, drow, act);
+    }
+  };
+  for (int kt = 0; kt < mine; ++kt) {
+    body(kt, us, ud, nus, nud);
+#pragma unroll
+    for (int q = 0; q < kColEdges; ++q) { us[q] = nus[q]; ud[q] = nud[q]; }
   }
   const int ops[2] = {OP_MAX, OP_SUM};
   reduce_and_finalize<2>(acc, ops, part, counter, c, A_COL);

@@ -367,6 +367,7 @@ void init_ctx_common(mwu_ctx* c, const mwu_options* opt) {
   }
   CK(cudaFuncSetAttribute(search_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSearchSmem));
   CK(cudaFuncSetAttribute(col_densest_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kColSmem));
+  CK(cudaFuncSetAttribute(col_match_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMSmem));
   CK(cudaMemsetAsync(c->counter, 0, sizeof(unsigned int), c->st));
   CK(cudaEventCreate(&c->ev0));
   CK(cudaEventCreate(&c->ev1));
@@ -654,10 +655,10 @@ void build_blocked_order(mwu_ctx* c) {
   unsigned long long *keys = talloc<unsigned long long>(E), *kout = talloc<unsigned long long>(E);
   uint32_t* vals = talloc<uint32_t>(E);
   c->perm = dalloc<uint32_t>(c, E);
-  k_block_keys<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->src, c->dst, prowf, nbR, kBlockL, kBlockR, keys, vals);
-  CKL();
   int bits = kBlockL + kBlockR;
+  k_block_keys<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->src, c->dst, prowf, nbR, kBlockL, kBlockR, keys, vals);
   while (bits < 64 && (1ull << (bits - kBlockL - kBlockR)) < (unsigned long long)nbL * (unsigned long long)nbR) ++bits;
+  CKL();
   size_t tb = 0;
   CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, kout, vals, c->perm, E, 0, bits, c->st));
   void* t = talloc<char>(tb);
@@ -866,11 +867,11 @@ void enqueue_column(mwu_ctx* c, cudaStream_t st) {
     case K_MATCH:
       if (c->scatterP) {
         CK(cudaMemsetAsync(c->dy, 0, (c->mP > 0 ? c->mP : 1) * sizeof(double), st));
-        const int64_t blocks = (c->E + MWU_MATCH_U * MWU_NT - 1) / (MWU_MATCH_U * MWU_NT);
-        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(blocks, MWU_MATCH_MINB * c->sms));
-        col_match_fast<<<g, MWU_NT, 0, st>>>(c->E, c->srow, c->drow, c->u, c->x, c->d, c->dy,
-                                            c->record ? c->gdbg : nullptr, c->record ? c->hdbg : nullptr,
-                                            c->ctl, c->part, c->counter, c->act);
+        const int64_t tiles = (c->E + MWU_CT - 1) / MWU_CT;
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, MWU_MT_MINB * c->sms));
+        col_match_fast<<<g, MWU_NT, kMSmem, st>>>(c->E, c->srow, c->drow, c->u, c->x, c->d, c->dy,
+                                                c->record ? c->gdbg : nullptr, c->record ? c->hdbg : nullptr,
+                                                c->ctl, c->part, c->counter, c->act);
         c->launches++;
         break;
       }
