@@ -158,6 +158,8 @@ typedef struct {
   double max_Px_raw, min_Cx_raw;     /* max y and min z of the feasible probe's final iterate x    */
   double max_Px, min_Cx;             /* the same for the returned x_out = x / min(Cx) (Q15):        */
                                      /* max_Px = certificate, min_Cx = 1; NaN if none               */
+  int64_t probe_graph;               /* 1: the probe loop ran as one CUDA-graph launch per probe   */
+                                     /* (one GPU, or sharded over NCCL); 0: host-driven iterations  */
 } mwu_stats;
 
 /* Vector ids for mwu_get_vec (per-iteration parity, BASELINE north_star): */

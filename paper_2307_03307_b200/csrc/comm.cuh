@@ -9,9 +9,12 @@
 //
 //  * NcclComm: NCCL over NVLink / NVSwitch, loaded with dlopen (libnccl.so.2 of the PyTorch
 //    wheel, or $MWU_NCCL_LIB) so that a single-GPU run has no NCCL dependency.
+//    NCCL collectives are stream-ordered device work, so the sharded probe loop is captured
+//    into the same CUDA graph as the one-GPU loop (conditional WHILE nodes).
 //  * SimComm: an in-process group of `world` contexts on ONE device (one host thread per rank,
 //    host-side barriers, device copies / sums issued by rank 0 in rank order).  No kernel ever
-//    waits on another; it exists so that the sharded engine is testable on a one-GPU box.
+//    waits on another; it exists so that the sharded engine is testable on a one-GPU box.  Its
+//    barriers are host work, so SimComm runs are host-driven (not captured).
 #pragma once
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -34,6 +37,8 @@ struct Comm {
   virtual void allreduce_sum(double* buf, int64_t n, cudaStream_t st) = 0;
   // out[r * n + i] = in_r[i] for every rank r
   virtual void allgather(const double* in, double* out, int64_t n, cudaStream_t st) = 0;
+  // collectives may be captured into a CUDA graph (enqueued on the stream, no host work)
+  virtual bool capturable() const { return false; }
 };
 
 // ---------------------------------------------------------------------------------- NCCL
@@ -93,6 +98,7 @@ struct NcclComm : Comm {
     L.check(L.commInitRank(&c, w, id, r), "ncclCommInitRank");
   }
   ~NcclComm() override { if (c) NcclLib::get().commDestroy(c); }
+  bool capturable() const override { return true; }
   // a failed collective aborts the communicator (pending operations on every rank return
   // instead of hanging) before the error reaches the caller as MWU_ERR_NCCL
   void checked(int r, const char* what) {

@@ -113,6 +113,7 @@ struct Ctl {
   // ---- multi-GPU: partial phase reductions are deferred to the host-driven exchange
   int32_t world, dpending;             // ranks; a deferred reduction awaits finalize_multi
   int32_t repvars, partupd;            // variables replicated (vcover / domset); update reduction partial
+  int32_t ownrows, pad_own;            // owner-partitioned packing rows (sharded bipartite matching)
   int32_t dn, daction;                 // its slot count and action
   double dslots[MWU_SLOTS];            // this rank's reduced slots
   int32_t dops[MWU_SLOTS];             // their combine ops

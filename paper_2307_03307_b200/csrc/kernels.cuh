@@ -499,7 +499,7 @@ __device__ void finalize(Ctl* c, int action, double* r) {
       c->alpha_last = c->alpha; c->alpha_prev = c->alpha; c->apply_prev = 1;
       if (near_tie(c->cSing ? c->zS + c->alpha * c->dzS : c->newsC, 1.0)) c->near_ties++;   // min z >= 1
       if (c->pSing) { c->yS = c->yS + c->alpha * c->dyS; c->sP = c->yS; c->SP = 1.0; }
-      else { c->sP = c->newsP; c->SP = r[0]; }
+      else { c->sP = c->newsP; c->SP = r[0] + r[2]; }          // r[2]: owned rows (0 unless sharded by owner)
       if (c->cSing) { c->zS = c->zS + c->alpha * c->dzS; c->sC = c->zS; c->SC = 1.0; }
       else if (c->lazyC) { c->sC = c->newsC; c->SC = c->acc_tc * exp(c->eta * (c->newsC - c->acc_sh)); }
       else { c->sC = c->newsC; c->SC = r[1]; }
@@ -519,7 +519,7 @@ __device__ void finalize(Ctl* c, int action, double* r) {
       c->sC = c->cSing ? c->zS : r[1];
       break;
     case A_INIT_W: {
-      c->SP = c->pSing ? 1.0 : r[0];
+      c->SP = c->pSing ? 1.0 : r[0] + r[2];
       c->SC = c->cSing ? 1.0 : r[1];
       if (!(isfinite(c->SP) && isfinite(c->SC) && c->SP > 0.0 && c->SC > 0.0)) {
         c->nan_flag = 1; c->status = ST_INFEASIBLE;
@@ -547,7 +547,8 @@ __device__ void finalize(Ctl* c, int action, double* r) {
 // finalize_multi combines them in rank order and runs the same control logic on every rank.
 __device__ __forceinline__ bool partial_action(const Ctl* c, int a) {
   if (a == A_COL || a == A_INIT_SING || a == A_SUM) return !c->repvars;   // over the (local) variables
-  if (a == A_UPDATE) return c->partupd;                                  // local covering rows
+  if (a == A_UPDATE) return c->partupd;                                  // local covering / owned rows
+  if (a == A_STEP_DONE + 100) return c->ownrows;                         // max d^(y) over owned rows
   return a == A_COL_FAST || a == A_SEARCH || a == A_INIT_EXT || a == A_INIT_W || a == A_VI_EXACT;
 }
 __device__ void finish(Ctl* c, int action, double* res, const int* ops, int n) {
@@ -1254,6 +1255,7 @@ constexpr size_t kSearchSmem = (size_t)MWU_SST * 3 * MWU_SCH * sizeof(double);
 
 struct SearchArgs {
   int64_t mP; const double *y, *dy, *u;                  // this rank's slice of the packing rows
+  int64_t mP2; const double *y2, *dy2, *u2;              // + its own rows (owner-partitioned sharding)
   int64_t mC; const double *z, *dz, *v;                  // dense covering rows (v: weights)
   const double *rz, *rdz, *rv; const int32_t* tcnt; int64_t nstreams, rcap;   // compacted (rz != nullptr)
   const double* emtab;                                   // 768: T, T-1 hi, T-1 lo (fastmath.cuh)
@@ -1271,6 +1273,7 @@ __device__ __forceinline__ void search_body_fast(const SearchArgs& A, const Cand
   {
     PRowFast<PT, NC, SQ1> f(K, c->eta, tab);
     if (!c->pSing) stream_rows3(A.y, A.dy, A.u, A.mP, sbuf, bars, it, f);
+    if (!c->pSing && A.mP2 > 0) stream_rows3(A.y2, A.dy2, A.u2, A.mP2, sbuf, bars, it, f);
     block_partials<NC>(f.ep, opsS, part, R_EP(0));
     block_partials<NC>(f.ep, opsS, part, R_LP(0));          // LSE-mode candidates read this slot
     block_partials<NC>(f.mx, opsX, part, R_MX(0));
@@ -1300,6 +1303,7 @@ __device__ __forceinline__ void search_body_gen(const SearchArgs& A, const Cands
   {
     PRowGen f(K, c->eta);
     if (!c->pSing) stream_rows3(A.y, A.dy, A.u, A.mP, sbuf, bars, it, f);
+    if (!c->pSing && A.mP2 > 0) stream_rows3(A.y2, A.dy2, A.u2, A.mP2, sbuf, bars, it, f);
     nd[0] = f.nd;
     block_partials<MWU_MAXC>(f.ep, opsS, part, R_EP(0));
     block_partials<MWU_MAXC>(f.lp, opsS, part, R_LP(0));
@@ -1381,17 +1385,20 @@ __global__ void __launch_bounds__(MWU_NT, MWU_SEARCH_MINB) search_pass(SearchArg
 // y += alpha d^(y), z += alpha d^(z) fused with u = exp(eta (y - s_P)),
 // v = exp(-eta (z - s_C)) at the accepted alpha's shifts, and S_P, S_C.
 // has_delta = 0: initial weights only (init) with shifts from A_INIT_EXT.
+// Packing rows [0, mP) — or, on an owner-partitioned sharded matching, the
+// replicated rows [0, mP) plus this rank's own rows [R0, R1), whose weight sum goes to slot 2.
 __global__ void __launch_bounds__(MWU_NT) update_rows(int64_t mP, double* __restrict__ y, const double* __restrict__ dy,
                                                       double* __restrict__ u, int64_t mC, double* __restrict__ z,
                                                       const double* __restrict__ dz, double* __restrict__ v, Ctl* c,
-                                                      double* part, unsigned int* counter, int has_delta) {
+                                                      double* part, unsigned int* counter, int has_delta,
+                                                      int64_t R0, int64_t R1) {
   if (c->status != ST_RUNNING) {
     if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(c->h_iter, 0u);
     return;
   }
   const double a = c->alpha, eta = c->eta, neta = -c->eta;
   const double sP = has_delta ? c->newsP : c->sP, sC = has_delta ? c->newsC : c->sC;
-  double acc[2] = {0.0, 0.0};
+  double acc[3] = {0.0, 0.0, 0.0};
   const int64_t stride = (int64_t)gridDim.x * MWU_NT;
   const int64_t tid = (int64_t)blockIdx.x * MWU_NT + threadIdx.x;
   for (int64_t i = tid; i < mP; i += stride) {
@@ -1401,6 +1408,13 @@ __global__ void __launch_bounds__(MWU_NT) update_rows(int64_t mP, double* __rest
     if (u) u[i] = w;
     acc[0] += w;
   }
+  for (int64_t i = R0 + tid; i < R1; i += stride) {
+    double yi = y[i];
+    if (has_delta) { yi = yi + a * dy[i]; y[i] = yi; }
+    const double w = exp(eta * (yi - sP));
+    if (u) u[i] = w;
+    acc[2] += w;
+  }
   for (int64_t i = tid; i < mC; i += stride) {
     double zi = z[i];
     if (has_delta) { zi = zi + a * dz[i]; z[i] = zi; }
@@ -1408,8 +1422,8 @@ __global__ void __launch_bounds__(MWU_NT) update_rows(int64_t mP, double* __rest
     if (v) v[i] = w;
     acc[1] += w;
   }
-  const int ops[2] = {OP_SUM, OP_SUM};
-  reduce_and_finalize<2>(acc, ops, part, counter, c, has_delta ? A_UPDATE : A_INIT_W);
+  const int ops[3] = {OP_SUM, OP_SUM, OP_SUM};
+  reduce_and_finalize<3>(acc, ops, part, counter, c, has_delta ? A_UPDATE : A_INIT_W);
 }
 
 // Init: shifts s_P = max y, s_C = min z (Q4).
@@ -1452,6 +1466,13 @@ __global__ void flush_x(int64_t n, double* __restrict__ x, const double* __restr
 }
 
 // out = in / s  with s = *sp (x_out = x / min(Cx), Q15), or out = in / S (w = u / S).
+// owner-partitioned rows: keep the replicated prefix [0, nL) on rank 0 only and the own rows
+// [R0, R1); zeros elsewhere (a sum over ranks then assembles the whole vector exactly)
+__global__ void own_mask(int64_t m, const double* __restrict__ in, double* __restrict__ out, int64_t nL, int64_t R0,
+                         int64_t R1, int keep_prefix) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = ((i < nL && keep_prefix) || (i >= R0 && i < R1)) ? in[i] : 0.0;
+}
 __global__ void scale_div(int64_t n, const double* __restrict__ in, double* __restrict__ out, const double* sp) {
   const double s = *sp;
   for (int64_t i = (int64_t)blockIdx.x * MWU_NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * MWU_NT)

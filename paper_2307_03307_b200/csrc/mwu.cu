@@ -95,6 +95,11 @@ struct mwu_ctx {
   Comm* comm = nullptr;
   int64_t Eg = 0, ng = 0, mCg = 0, e0 = 0;   // global edges / variables / covering rows
   std::vector<int64_t> rb;                    // [world+1] ranges of the sharded dimension
+  // owner-partitioned bipartite matching (sharded): right rows [own_rows[r], own_rows[r+1]) and
+  // the internal edges [own_rb[r], own_rb[r+1]) belong to rank r; rows [0, nLx) are replicated
+  int own = 0;
+  int64_t nLx = 0, R0 = 0, R1 = 0;
+  std::vector<int64_t> own_rows, own_rb;
   int64_t r0 = 0, k0 = 0, nnzL = 0;           // domset: first local row, first local nonzero, count
   uint32_t* perm_full = nullptr;
   double* gslots = nullptr;                   // [world][MWU_SLOTS] gathered reduction slots
@@ -335,13 +340,15 @@ void init_ctx_common(mwu_ctx* c, const mwu_options* opt) {
   // group is passed (the sharded engine with one rank: exercises the exchange plumbing)
   if (c->world > 1 || c->opt.nccl_id || c->opt.comm_group) {
     if (c->rank < 0 || c->rank >= c->world) throw MwuError{MWU_ERR_ARG, "rank out of range"};
-    c->opt.use_graph = 0;                    // collectives are host-orchestrated
     try {
       if (c->opt.comm_group) c->comm = new SimComm((SimGroup*)c->opt.comm_group, c->rank);
       else if (c->opt.nccl_id) c->comm = new NcclComm(c->world, c->rank, c->opt.nccl_id);
       else throw std::runtime_error("world > 1 needs nccl_id or comm_group");
       c->sharded = 1;
     } catch (const std::exception& e) { throw MwuError{MWU_ERR_NCCL, e.what()}; }
+    // NCCL collectives are captured into the probe graph with the kernels; the in-process test
+    // group synchronises on the host, so its runs are host-driven
+    if (!c->comm->capturable()) c->opt.use_graph = 0;
   }
   if (c->opt.device >= 0) CK(cudaSetDevice(c->opt.device));
   CK(cudaGetDevice(&c->dev));
@@ -569,11 +576,13 @@ void localize(mwu_ctx* c) {
     c->nnzL = rp[c->r0 + c->mC] - c->k0;
     return;                                    // variables (vertices) replicated
   }
-  for (int r = 0; r <= c->world; ++r) {
-    int64_t a, b;
-    shard_range(c->Eg, c->world, std::min(r, c->world - 1), a, b);
-    c->rb[r] = (r == c->world) ? c->Eg : a;
-  }
+  if (c->own) c->rb = c->own_rb;              // edges of the rank's own right rows
+  else
+    for (int r = 0; r <= c->world; ++r) {
+      int64_t a, b;
+      shard_range(c->Eg, c->world, std::min(r, c->world - 1), a, b);
+      c->rb[r] = (r == c->world) ? c->Eg : a;
+    }
   const int64_t a = c->rb[c->rank], b = c->rb[c->rank + 1];
   c->e0 = a;
   c->E = b - a;
@@ -585,9 +594,22 @@ void localize(mwu_ctx* c) {
   }
   c->n = w * c->E;
   if (c->kind == K_DENSEST) c->mC = c->E;
+  c->perm += a;
+  if (c->own) {
+    // owner edge ranges are not tile-aligned: the local rows move to aligned buffers (the
+    // column kernel bulk-copies them), and the rank's rows are [0, nLx) + [R0, R1)
+    int32_t *sr = dalloc<int32_t>(c, c->E), *dr = dalloc<int32_t>(c, c->E);
+    if (c->E > 0) {
+      CK(cudaMemcpyAsync(sr, c->srow + a, c->E * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->st));
+      CK(cudaMemcpyAsync(dr, c->drow + a, c->E * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->st));
+    }
+    c->srow = sr; c->drow = dr;
+    c->R0 = std::max(c->own_rows[c->rank], c->nLx);
+    c->R1 = std::max(c->own_rows[c->rank + 1], c->R0);
+    return;
+  }
   c->srow += a;
   c->drow += a;
-  c->perm += a;
 }
 
 // full vector of a sharded quantity (w per item of the sharded dimension: edges, or domset
@@ -632,9 +654,10 @@ void build_blocked_order(mwu_ctx* c) {
   if (kBlockL > 31 || kBlockR > 31) throw MwuError{MWU_ERR_ARG, "block_l / block_r must be <= 31"};
   // packing rows in degree-descending order (fast path only; hooks restore vertex order)
   int32_t* prowf = talloc<int32_t>(c->nv);
+  uint32_t* dvo = talloc<uint32_t>(c->nv);   // vertices in row order
   {
     unsigned long long *dk = talloc<unsigned long long>(c->nv), *dko = talloc<unsigned long long>(c->nv);
-    uint32_t *dv = talloc<uint32_t>(c->nv), *dvo = talloc<uint32_t>(c->nv);
+    uint32_t *dv = talloc<uint32_t>(c->nv);
     k_deg_keys<<<grid_for(c, c->nv), MWU_NT, 0, c->st>>>(c->nv, c->deg, c->kind == K_MATCH ? c->nleft : 0, dk, dv);
     CKL();
     size_t tb2 = 0;
@@ -645,7 +668,7 @@ void build_blocked_order(mwu_ctx* c) {
     k_deg_rows<<<grid_for(c, c->nprime), MWU_NT, 0, c->st>>>(c->nprime, dvo, c->prow, prowf, c->rowperm);
     CKL();
     sync(c);
-    tfree(t2); tfree(dk); tfree(dko); tfree(dv); tfree(dvo);
+    tfree(t2); tfree(dk); tfree(dko); tfree(dv);
   }
   // L2 blocks over ROW ranges of the (degree-ordered) packing-row vectors: key = (srow >> BL,
   // drow >> BR, srow, drow)
@@ -656,8 +679,53 @@ void build_blocked_order(mwu_ctx* c) {
   uint32_t* vals = talloc<uint32_t>(E);
   c->perm = dalloc<uint32_t>(c, E);
   int bits = kBlockL + kBlockR;
-  k_block_keys<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->src, c->dst, prowf, nbR, kBlockL, kBlockR, keys, vals);
-  while (bits < 64 && (1ull << (bits - kBlockL - kBlockR)) < (unsigned long long)nbL * (unsigned long long)nbR) ++bits;
+  int64_t* d_ob = nullptr;
+  if (c->own) {
+    // right rows split into W ranges of about E / W edges each (degree prefix sums), boundaries
+    // even (16-byte aligned row slices for the search's bulk copies)
+    const int W = c->world;
+    unsigned long long* cnt = talloc<unsigned long long>(1);
+    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), c->st));
+    k_count_left<<<grid_for(c, c->nleft), MWU_NT, 0, c->st>>>(c->nleft, c->deg, cnt);
+    CKL();
+    const int64_t nLp = (int64_t)read_scalar(c, cnt);
+    tfree(cnt);
+    const int64_t nR = c->nprime - nLp;
+    int64_t *rd = talloc<int64_t>(std::max<int64_t>(nR, 1)), *cum = talloc<int64_t>(std::max<int64_t>(nR, 1));
+    k_right_deg<<<grid_for(c, std::max<int64_t>(nR, 1)), MWU_NT, 0, c->st>>>(nR, nLp, dvo, c->deg, rd);
+    CKL();
+    size_t tb3 = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tb3, rd, cum, nR, c->st));
+    void* t3 = talloc<char>(tb3);
+    CK(cub::DeviceScan::InclusiveSum(t3, tb3, rd, cum, nR, c->st));
+    int64_t* d_b = talloc<int64_t>(W + 1);
+    if (W > 1) k_owner_bounds<<<1, 64, 0, c->st>>>(cum, nR, E, W, d_b);
+    CKL();
+    std::vector<int64_t> hb(W + 1, 0);
+    CK(cudaMemcpyAsync(hb.data(), d_b, (W + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    tfree(t3); tfree(rd); tfree(cum); tfree(d_b);
+    c->nLx = std::min(c->nprime, nLp + (nLp & 1));
+    c->own_rows.assign(W + 1, 0);
+    c->own_rows[0] = nLp;
+    for (int r = 1; r < W; ++r) {
+      int64_t row = nLp + hb[r] + 1;                       // the row reaching the target stays below
+      row = (row + 1) & ~int64_t(1);
+      c->own_rows[r] = std::min(c->nprime, std::max(row, std::max(c->own_rows[r - 1], c->nLx)));
+    }
+    c->own_rows[W] = c->nprime;
+    int64_t maxrows = 1;
+    for (int r = 0; r < W; ++r) maxrows = std::max(maxrows, c->own_rows[r + 1] - c->own_rows[r]);
+    const int nbRo = (int)((maxrows + (int64_t(1) << kBlockR) - 1) >> kBlockR);
+    d_ob = talloc<int64_t>(W + 1);
+    CK(cudaMemcpyAsync(d_ob, c->own_rows.data(), (W + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->st));
+    k_block_keys_own<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->src, c->dst, prowf, d_ob, W, nbRo, kBlockL, kBlockR,
+                                                          keys, vals);
+    while (bits < 64 && (1ull << (bits - kBlockL - kBlockR)) < (unsigned long long)W * (unsigned long long)nbRo) ++bits;
+  } else {
+    k_block_keys<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->src, c->dst, prowf, nbR, kBlockL, kBlockR, keys, vals);
+    while (bits < 64 && (1ull << (bits - kBlockL - kBlockR)) < (unsigned long long)nbL * (unsigned long long)nbR) ++bits;
+  }
   CKL();
   size_t tb = 0;
   CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys, kout, vals, c->perm, E, 0, bits, c->st));
@@ -665,8 +733,20 @@ void build_blocked_order(mwu_ctx* c) {
   CK(cub::DeviceRadixSort::SortPairs(t, tb, keys, kout, vals, c->perm, E, 0, bits, c->st));
   k_map_endpoints_perm<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->perm, c->src, c->dst, prowf, c->srow, c->drow);
   CKL();
+  if (c->own) {                              // edge range of every owner along the internal order
+    k_orient<<<grid_for(c, E), MWU_NT, 0, c->st>>>(E, c->srow, c->drow);
+    CKL();
+    const int W = c->world;
+    int64_t* d_e = talloc<int64_t>(W + 1);
+    k_owner_edges<<<1, 128, 0, c->st>>>(c->drow, E, d_ob, W, d_e);
+    CKL();
+    c->own_rb.assign(W + 1, 0);
+    CK(cudaMemcpyAsync(c->own_rb.data(), d_e, (W + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, c->st));
+    sync(c);
+    tfree(d_e); tfree(d_ob);
+  }
   sync(c);
-  tfree(prowf);
+  tfree(prowf); tfree(dvo);
   tfree(t); tfree(keys); tfree(kout); tfree(vals);
 }
 
@@ -1024,12 +1104,15 @@ void enqueue_search(mwu_ctx* c, cudaStream_t st) {
   const int g = (int)std::max<int64_t>(1, std::min<int64_t>(MWU_SEARCH_MINB * c->sms, chunks));
   SearchArgs A;
   int64_t p0 = 0, p1 = c->mP;                // sharded: each rank sums a slice of the replicated rows
+  const int64_t rep = c->own ? c->nLx : c->mP;
   if (c->sharded) {
-    shard_range(c->mP, c->world, c->rank, p0, p1);
+    shard_range(rep, c->world, c->rank, p0, p1);
     p0 &= ~int64_t(1);                       // 16-byte aligned bulk copies
     if (c->rank + 1 < c->world) p1 &= ~int64_t(1);
   }
   A.mP = p1 - p0; A.y = c->y + p0; A.dy = c->dy + p0; A.u = c->u + p0;
+  A.mP2 = c->own ? c->R1 - c->R0 : 0;       // + the rank's own rows (owner-partitioned matching)
+  A.y2 = c->y + c->R0; A.dy2 = c->dy + c->R0; A.u2 = c->u + c->R0;
   A.mC = c->mC; A.z = c->z; A.dz = c->dz; A.v = c->v;
   A.rz = c->rz; A.rdz = c->rdz; A.rv = c->rv; A.tcnt = c->tcnt;
   A.nstreams = c->rec_grid * (MWU_NT / 32); A.rcap = c->rec_cap;
@@ -1042,12 +1125,18 @@ void enqueue_update(mwu_ctx* c, cudaStream_t st, int has_delta) {
   // lazyC: the covering side is updated lazily by the next column kernel (only at init are its
   // weight sums formed here, without storing v)
   const int64_t mC = (c->lazyC && has_delta) ? 0 : c->mC;
-  update_rows<<<rows_grid(c, c->mP + mC), MWU_NT, 0, st>>>(c->mP, c->y, c->dy, c->u, mC, c->z, c->dz, c->v,
-                                                          c->ctl, c->part, c->counter, has_delta);
+  const int64_t mP = c->own ? c->nLx : c->mP;   // owner-partitioned: replicated rows + own rows
+  update_rows<<<rows_grid(c, c->mP + mC), MWU_NT, 0, st>>>(mP, c->y, c->dy, c->u, mC, c->z, c->dz, c->v,
+                                                          c->ctl, c->part, c->counter, has_delta,
+                                                          c->own ? c->R0 : 0, c->own ? c->R1 : 0);
   c->launches++;
 }
 
 // ------------------------------------------------------------------------------ graph (probe loop)
+void enqueue_col_step(mwu_ctx* c);
+void enqueue_search_pass(mwu_ctx* c);
+void enqueue_update_phase(mwu_ctx* c);
+
 void build_probe_graph(mwu_ctx* c) {
   if (c->graph_ok) return;
   cudaGraph_t top;
@@ -1067,8 +1156,7 @@ void build_probe_graph(mwu_ctx* c) {
   // part A: column + step
   const int64_t l0 = c->launches;
   CK(cudaStreamBeginCaptureToGraph(c->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  enqueue_column(c, c->st);
-  enqueue_forward(c, c->st, c->d, c->dy, c->dz, false);
+  enqueue_col_step(c);
   cudaStreamCaptureStatus cst;
   const cudaGraphNode_t* deps = nullptr;
   size_t ndeps = 0;
@@ -1086,11 +1174,11 @@ void build_probe_graph(mwu_ctx* c) {
   CK(cudaGraphAddNode(&sn, body, leaf.data(), leaf.size(), &p2));
   cudaGraph_t sbody = p2.conditional.phGraph_out[0];
   CK(cudaStreamBeginCaptureToGraph(c->st, sbody, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  enqueue_search(c, c->st);
+  enqueue_search_pass(c);
   CK(cudaStreamEndCapture(c->st, &g2));
   // part C: update, after the search loop
   CK(cudaStreamBeginCaptureToGraph(c->st, body, &sn, nullptr, 1, cudaStreamCaptureModeRelaxed));
-  enqueue_update(c, c->st, 1);
+  enqueue_update_phase(c);
   CK(cudaStreamEndCapture(c->st, &g2));
   CK(cudaGraphInstantiate(&c->gexec, top, 0));
   c->graph = top;
@@ -1131,7 +1219,8 @@ void probe_begin(mwu_ctx* c, double bound, double eps) {
   h.compC = c->compC;
   h.world = c->sharded ? std::max(2, c->world) : 1;   // device: defer partial reductions when sharded
   h.repvars = c->fastC ? 1 : 0;                          // covering kinds: variables replicated
-  h.partupd = (c->sharded && c->fastC) ? 1 : 0;          // their covering rows are local
+  h.partupd = ((c->sharded && c->fastC) || c->own) ? 1 : 0;   // their covering rows / owned rows are local
+  h.ownrows = c->own;
   for (int i = 0; i < 32; ++i) h.aguess[i] = c->aguess[i];
   h.status = c->empty_cover ? ST_INFEASIBLE : ST_RUNNING;
   h.reason = c->empty_cover ? R_EMPTY_COVER : R_NONE;
@@ -1155,7 +1244,7 @@ void probe_begin(mwu_ctx* c, double bound, double eps) {
   exchange(c);
   // y = P x, z = C x
   enqueue_forward(c, c->st, c->x, c->y, c->z, true);
-  if (c->scatterP) allreduce_rows(c, c->y, c->mP);   // sharded: partial packing rows of the local edges
+  if (c->scatterP) allreduce_rows(c, c->y, c->own ? c->nLx : c->mP);   // sharded: partial rows of the local edges
   init_ext<<<rows_grid(c, c->mP + c->mC), MWU_NT, 0, c->st>>>(c->mP, c->y, c->mC, c->z, c->ctl, c->part, c->counter);
   c->launches++;
   exchange(c);
@@ -1168,14 +1257,12 @@ void probe_begin(mwu_ctx* c, double bound, double eps) {
   c->eps = eps;
 }
 
-// host-driven iteration (debug / lockstep parity path); alpha > 0 fixes the step
-void host_iteration(mwu_ctx* c, double alpha) {
-  push_field(c, &c->ctl->fixed_alpha, alpha > 0.0 ? alpha : 0.0);
-  pull_ctl(c);
-  if (c->hctl->status != ST_RUNNING) return;
+// The phases of one MWU iteration as stream work (host-driven loop and probe-graph capture
+// alike).  Sharded runs add the exchange steps: on the graph path (NCCL) they are captured too.
+void enqueue_col_step(mwu_ctx* c) {          // column + forward products
   enqueue_column(c, c->st);
   if (c->sharded && c->scatterP) {
-    allreduce_rows(c, c->dy, c->mP);         // the one vector exchange per iteration
+    allreduce_rows(c, c->dy, c->own ? c->nLx : c->mP);   // the one vector exchange per iteration
     exchange(c);                             // column reductions (max d, sums, inactive rows)
     if (c->lazyC) {
       inactive_exact<<<rows_grid(c, c->E), MWU_NT, 0, c->st>>>(c->E, c->act, c->z, c->ctl, c->part, c->counter);
@@ -1183,16 +1270,31 @@ void host_iteration(mwu_ctx* c, double alpha) {
     }
   }
   enqueue_forward(c, c->st, c->d, c->dy, c->dz, false);
+  if (c->own) exchange(c);                   // max d^(y) over the owned rows
+}
+void enqueue_search_pass(mwu_ctx* c) {       // one HBM pass of the step search
+  enqueue_search(c, c->st);
+  exchange(c);
+}
+void enqueue_update_phase(mwu_ctx* c) {      // y, z, weights of the accepted step
+  enqueue_update(c, c->st, 1);
+  exchange(c);                               // sharded covering kinds: S_C over local rows
+}
+
+// host-driven iteration (debug / lockstep parity path); alpha > 0 fixes the step
+void host_iteration(mwu_ctx* c, double alpha) {
+  push_field(c, &c->ctl->fixed_alpha, alpha > 0.0 ? alpha : 0.0);
+  pull_ctl(c);
+  if (c->hctl->status != ST_RUNNING) return;
+  enqueue_col_step(c);
   CKL();
   for (int guard = 0; guard < 100000; ++guard) {
     pull_ctl(c);
     if (c->hctl->status != ST_RUNNING || !c->hctl->sactive) break;
-    enqueue_search(c, c->st);
-    exchange(c);
+    enqueue_search_pass(c);
     CKL();
   }
-  enqueue_update(c, c->st, 1);
-  exchange(c);                               // sharded covering kinds: S_C over local rows
+  enqueue_update_phase(c);
   CKL();
   sync(c);
   if (alpha > 0.0) push_field(c, &c->ctl->fixed_alpha, 0.0);
@@ -1259,7 +1361,7 @@ void profile_iters(mwu_ctx* c, int64_t k, double* out) {
     timed(0, [&] {
       enqueue_column(c, c->st);
       if (c->sharded && c->scatterP) {
-        allreduce_rows(c, c->dy, c->mP);
+        allreduce_rows(c, c->dy, c->own ? c->nLx : c->mP);
         exchange(c);
         if (c->lazyC) {
           inactive_exact<<<rows_grid(c, c->E), MWU_NT, 0, c->st>>>(c->E, c->act, c->z, c->ctl, c->part, c->counter);
@@ -1267,7 +1369,10 @@ void profile_iters(mwu_ctx* c, int64_t k, double* out) {
         }
       }
     });
-    timed(1, [&] { enqueue_forward(c, c->st, c->d, c->dy, c->dz, false); });
+    timed(1, [&] {
+      enqueue_forward(c, c->st, c->d, c->dy, c->dz, false);
+      if (c->own) exchange(c);
+    });
     for (int guard = 0; guard < 100000; ++guard) {
       pull_ctl(c);
       if (c->hctl->status != ST_RUNNING || !c->hctl->sactive) break;
@@ -1448,6 +1553,7 @@ void solve(mwu_ctx* c, double eps, int64_t max_iter, int32_t* outcome) {
   S.t_solve_ms = ms;
   S.t_loop_ms = loop_ms_total;
   S.kernel_launches = c->launches - l0;
+  S.probe_graph = c->opt.use_graph ? 1 : 0;
 }
 
 void fill_static_stats(mwu_ctx* c) {
@@ -1573,6 +1679,8 @@ mwu_status mwu_create_graph(const mwu_graph* g, const mwu_options* opt, mwu_ctx*
         c->nnzP = 2 * c->E; c->nnzC = 2 * c->E; c->empty_dropped = c->nv - c->nprime;
         break;
     }
+    // sharded bipartite matching: right rows owned by one rank each, only the left rows exchanged
+    c->own = (c->sharded && c->kind == K_MATCH && c->scatterP && c->nleft > 0) ? 1 : 0;
     if (c->scatterP) build_blocked_order(c);
     fill_static_stats(c);                    // global sizes
     if (c->sharded && !c->scatterP && !c->fastC)
@@ -1588,7 +1696,8 @@ mwu_status mwu_create_graph(const mwu_graph* g, const mwu_options* opt, mwu_ctx*
       memset(&h, 0, sizeof(Ctl));
       h.world = c->sharded ? std::max(2, c->world) : 1;
       h.repvars = c->fastC ? 1 : 0;
-      h.partupd = (c->sharded && c->fastC) ? 1 : 0;
+      h.partupd = ((c->sharded && c->fastC) || c->own) ? 1 : 0;
+      h.ownrows = c->own;
       CK(cudaMemcpyAsync(c->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, c->st));
       sync(c);
     }
@@ -1780,6 +1889,7 @@ mwu_status mwu_run_iters(mwu_ctx* c, int64_t k, int32_t* state) {
     c->stats.near_tie_count = c->hctl->near_ties;
     for (int p = 0; p < 4; ++p) c->stats.t_phase_ms[p] = c->hctl->tph[p] * 1e-6;
     c->stats.kernel_launches = c->launches - l0;
+    c->stats.probe_graph = c->opt.use_graph ? 1 : 0;
   } catch (const MwuError& e) { return fail(c, e); }
   return MWU_OK;
 }
@@ -1854,6 +1964,13 @@ mwu_status mwu_get_vec(mwu_ctx* c, int which, double* out, int64_t len) {
         }
         else { scale_div<<<rows_grid(c, c->mC), MWU_NT, 0, c->st>>>(c->mC, c->v, c->tmp, &c->ctl->SC); CKL(); src = c->tmp; }
         break;
+    }
+    if (c->own && !use_scal && (which == MWU_VEC_Y || which == MWU_VEC_DY || which == MWU_VEC_WP)) {
+      // every rank's own rows (replicated prefix from rank 0): zeros elsewhere, summed over ranks
+      own_mask<<<rows_grid(c, c->mP), MWU_NT, 0, c->st>>>(c->mP, src, c->tmp, c->nLx, c->R0, c->R1, c->rank == 0);
+      CKL();
+      allreduce_rows(c, c->tmp, c->mP);
+      src = c->tmp;
     }
     if (c->rowperm && !use_scal && (which == MWU_VEC_Y || which == MWU_VEC_DY || which == MWU_VEC_WP)) {
       k_unperm<<<grid_for(c, c->mP), MWU_NT, 0, c->st>>>(c->mP, c->rowperm, src, c->tmp2, 1);   // vertex order

@@ -119,6 +119,66 @@ __global__ void k_block_keys(int64_t E, const int32_t* src, const int32_t* dst, 
   }
 }
 
+// Owner-partitioned destination rows of a sharded bipartite matching: right
+// rows [ob[r], ob[r+1]) belong to rank r (ob[0] = first right row); key = (owner, dst block
+// within the owner's rows, src row, dst row), so each rank's edges are one contiguous range and
+// no other rank touches its right rows.
+__global__ void k_block_keys_own(int64_t E, const int32_t* src, const int32_t* dst, const int32_t* vrow,
+                                 const int64_t* ob, int W, int nbR, int BL, int BR, unsigned long long* keys,
+                                 uint32_t* vals) {
+  const unsigned long long mR = (1ull << BR) - 1ull;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p = vrow[src[e]], q = vrow[dst[e]];          // left rows come first: a left, b right
+    const unsigned long long a = (unsigned long long)(p < q ? p : q);
+    const int64_t b = p < q ? q : p;
+    int r = 0;
+    while (r + 1 < W && b >= ob[r + 1]) ++r;
+    const unsigned long long rel = (unsigned long long)(b - ob[0] < 0 ? 0 : b - ob[r]);
+    const unsigned long long blk = (unsigned long long)r * (unsigned long long)nbR + (rel >> BR);
+    keys[e] = (blk << (BL + BR)) | (a << BR) | (rel & mR);
+    vals[e] = (uint32_t)e;
+  }
+}
+// srow = the left endpoint's row, drow = the right endpoint's (rows of the left side come first)
+__global__ void k_orient(int64_t E, int32_t* srow, int32_t* drow) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t a = srow[i], b = drow[i];
+    if (a > b) { srow[i] = b; drow[i] = a; }
+  }
+}
+// number of non-isolated left vertices (their rows come first in the degree order)
+__global__ void k_count_left(int64_t nleft, const int32_t* deg, unsigned long long* out) {
+  unsigned long long k = 0;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nleft; v += (int64_t)gridDim.x * blockDim.x)
+    k += deg[v] > 0 ? 1ull : 0ull;
+  for (int o = 16; o > 0; o >>= 1) k += __shfl_down_sync(0xffffffffu, k, o);
+  if ((threadIdx.x & 31) == 0 && k) atomicAdd(out, k);
+}
+// degrees of the right rows in row order: rd[i] = deg[vertex of row nL + i]
+__global__ void k_right_deg(int64_t nR, int64_t nL, const uint32_t* vsorted, const int32_t* deg, int64_t* rd) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nR; i += (int64_t)gridDim.x * blockDim.x)
+    rd[i] = deg[vsorted[nL + i]];
+}
+// out[r] = first i with cum[i] >= target_r = r * total / W (r = 1 .. W-1), by binary search
+__global__ void k_owner_bounds(const int64_t* cum, int64_t n, int64_t total, int W, int64_t* out) {
+  const int r = threadIdx.x + 1;
+  if (r >= W) return;
+  const int64_t t = (int64_t)((__int128)total * r / W);
+  int64_t lo = 0, hi = n;
+  while (lo < hi) { const int64_t m = (lo + hi) / 2; if (cum[m] >= t) hi = m; else lo = m + 1; }
+  out[r] = lo;
+}
+// out[r] = first internal edge whose dst row is >= ob[r] (owners ascend along the internal order)
+__global__ void k_owner_edges(const int32_t* drow, int64_t E, const int64_t* ob, int W, int64_t* out) {
+  const int r = threadIdx.x;
+  if (r > W) return;
+  if (r == 0) { out[0] = 0; return; }
+  if (r == W) { out[W] = E; return; }
+  int64_t lo = 0, hi = E;
+  while (lo < hi) { const int64_t m = (lo + hi) / 2; if (drow[m] >= ob[r]) hi = m; else lo = m + 1; }
+  out[r] = lo;
+}
+
 // degree-descending row order (hot rows of power-law graphs cluster in a small, L2-resident
 // prefix of the packing-row vectors): key = (~deg, v)
 // (bipartite: the left side's rows first, so a source sweep never touches right-side rows)

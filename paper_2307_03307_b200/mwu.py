@@ -61,7 +61,7 @@ class Stats(ctypes.Structure):
                 ("bytes_alg_per_iter", ctypes.c_double), ("kernel_launches", ctypes.c_int64),
                 ("near_tie_count", ctypes.c_int64), ("t_phase_ms", ctypes.c_double * 4),
                 ("max_Px_raw", ctypes.c_double), ("min_Cx_raw", ctypes.c_double), ("max_Px", ctypes.c_double),
-                ("min_Cx", ctypes.c_double)]
+                ("min_Cx", ctypes.c_double), ("probe_graph", ctypes.c_int64)]
 
 
 EXPORTS = ["mwu_default_options", "mwu_create_csr", "mwu_create_graph", "mwu_solve", "mwu_get_x",

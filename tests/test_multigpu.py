@@ -196,22 +196,29 @@ def test_sharded_solve(cuda_ok, name):
 
 
 @pytest.mark.gpu
-def test_nccl_plumbing_one_rank(cuda_ok):
+@pytest.mark.parametrize("ci", range(len(CASES)))
+def test_nccl_plumbing_one_rank(cuda_ok, ci):
     """The NCCL communicator (dlopen'ed library, unique id through torch.distributed, allreduce
     and allgather on the library's stream) driving the sharded engine with one rank: the same
-    iterates as the plain engine.  (Several ranks need several GPUs; the sharding itself is
-    covered by the SimGroup tests above.)"""
+    iterates as the plain engine over 15 standard steps, and 12 searched iterations with the
+    collectives captured into the probe's CUDA graph (conditional WHILE nodes, device-side
+    Alg. 3 control, no host round trip per search pass) against the host-driven sharded loop
+    (in-process group of one rank): identical step sizes, iterates within 1e-10.  (The fast
+    paths reduce with fp64 atomics, so two runs agree to rounding, not bit for bit.  Several
+    ranks need several GPUs; the sharding itself is covered by the SimGroup tests above.)"""
     from paper_2307_03307_b200 import Solver
+    from paper_2307_03307_b200.mwu import SimGroup
     port = _free_port()
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
-        kind, G, eps = CASES[0]
+        kind, G, eps = CASES[ci]
         s, d = G.numpy()
         r = O.solve(kind, s, d, G.n_vertices, eps=eps, max_iter=300)
         B = [p[0] for p in r.probes if p[1] == O.FEASIBLE][-1]
         one = _solver(kind, G)
-        S = Solver.graph_distributed(kind, G.src.cuda(), G.dst.cuda(), G.n_vertices, 0)
+        nl = G.n_left if kind == "bmatch" else 0
+        S = Solver.graph_distributed(kind, G.src.cuda(), G.dst.cuda(), G.n_vertices, nl)
         for T in (one, S):
             T.probe_begin(B, eps)
             for _ in range(15):
@@ -219,7 +226,22 @@ def test_nccl_plumbing_one_rank(cuda_ok):
         for k in ("x", "y", "z", "d", "dy"):
             a, b = S.vec(k).cpu().numpy(), one.vec(k).cpu().numpy()
             assert np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)) <= 1e-10, k
+        grp = SimGroup(1)
+        H = _solver(kind, G, world=1, rank=0, comm_group=grp)
+        alphas = []
+        for T in (S, H):
+            T.probe_begin(B, eps)
+            T.run_iters(12)
+            alphas.append(T.scalars()["alpha_last"])
+        assert S.stats()["probe_graph"] == 1                # NCCL collectives inside the graph
+        assert H.stats()["probe_graph"] == 0                # host-driven reference
+        assert S.scalars()["t"] == H.scalars()["t"] and alphas[0] == alphas[1]
+        for k in ("x", "y", "z"):
+            a, b = S.vec(k).cpu().numpy(), H.vec(k).cpu().numpy()
+            assert np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)) <= 1e-10, k
         out = S.solve(eps, 300)
-        assert out == "feasible"
+        assert out == "feasible" and S.stats()["probe_graph"] == 1
+        del H
+        grp.close()
     finally:
         dist.destroy_process_group()
