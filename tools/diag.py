@@ -17,14 +17,21 @@ ap.add_argument("--iters", type=int, default=12)
 ap.add_argument("--use-graph", type=int, default=0)
 ap.add_argument("--active", type=int, default=1)
 ap.add_argument("--phases", type=int, default=0)
+ap.add_argument("--bound", type=float, default=0.0, help="probe bound (default: the first outer bisection bound)")
+ap.add_argument("--skip", type=int, default=0, help="iterations run through the probe graph before the listed ones")
 a = ap.parse_args()
 kind, eps, _ = bench.WORKLOADS[a.workload]
 G = gg.config_graph(a.workload, scale_down=a.scale_down, seed=1, device="cuda")
 gs = bench.graph_stats(G)
 S = Solver.graph(kind, G.src, G.dst, G.n_vertices, G.n_left if kind == "bmatch" else 0, use_graph=a.use_graph)
 L, H, _ = bench.bracket(kind, gs, eps)
-B = math.sqrt(L * H)
+B = a.bound if a.bound > 0 else math.sqrt(L * H)
 S.probe_begin(B, eps)
+if a.skip > 0:
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    S.run_iters(a.skip)        # use_graph=0 context: host-driven, but no per-iteration printing
+    torch.cuda.synchronize()
+    print(f"skipped {a.skip} iterations in {time.perf_counter() - t0:.1f} s", flush=True)
 print("stats", {k: v for k, v in S.stats().items() if k in ("n", "m_P", "m_C", "nnz_P", "nnz_C")}, "B", B, flush=True)
 for t in range(a.iters):
     sc0 = S.scalars()
