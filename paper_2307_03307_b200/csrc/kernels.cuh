@@ -1013,6 +1013,7 @@ __device__ __forceinline__ int grid_steps(int j) { return PT == PT_G16 ? (j == 0
 //   grid  a -> a + delta: expm1(x + w) = e + e_w + e e_w,  exp(x + w) = q q_w
 template <int PT, int NC, bool SQ1>
 struct PRowFast {
+  static constexpr double kAbsent = -INFINITY;     // y of an absent row (stream_rows3 pairs)
   double a[NC], ea0, ead, eta;
   int sq[NC];
   double ep[NC], mx[NC];
@@ -1026,9 +1027,47 @@ struct PRowFast {
       a[j] = k.a[j]; sq[j] = k.sq[j]; ep[j] = 0.0; mx[j] = -INFINITY; shP[j] = k.shP[j]; lse[j] = (k.mP[j] == CM_LSE);
     }
   }
+  __device__ __forceinline__ double xm1(double x) const {
+#if MWU_SEARCH_TAB
+    double em, q;
+    mwu_expm1_exp_tab(x, T, Mh, Ml, em, q);
+    return em;
+#else
+    return mwu_expm1(x);
+#endif
+  }
+  // two rows with their dependent chains interleaved; row 1 is masked by u1 = 0, y1 = -inf
+  __device__ __forceinline__ void pair(double y0, double d0, double u0, double y1, double d1, double u1) {
+    double e0 = xm1(ea0 * d0), e1 = xm1(ea0 * d1), ed0 = 0.0, ed1 = 0.0;
+    if (PT == PT_GRID || PT == PT_G16) { ed0 = xm1(ead * d0); ed1 = xm1(ead * d1); }
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      if (PT == PT_DOUBLE) {
+        if (SQ1) { if (j > 0) { e0 = e0 * (e0 + 2.0); e1 = e1 * (e1 + 2.0); } }
+        else { for (int s = 0; s < sq[j]; ++s) { e0 = e0 * (e0 + 2.0); e1 = e1 * (e1 + 2.0); } }
+      } else if (PT == PT_GRID) { e0 = e0 + ed0 + e0 * ed0; e1 = e1 + ed1 + e1 * ed1; }
+      else {
+#pragma unroll
+        for (int s = 0; s < grid_steps<PT>(j); ++s) { e0 = e0 + ed0 + e0 * ed0; e1 = e1 + ed1 + e1 * ed1; }
+      }
+      if (lse[j]) {
+        ep[j] += mwu_exp(eta * ((y0 + a[j] * d0) - shP[j]));
+        if (u1 != 0.0) ep[j] += mwu_exp(eta * ((y1 + a[j] * d1) - shP[j]));
+      } else ep[j] = __fma_rn(u1, e1, __fma_rn(u0, e0, ep[j]));
+    }
+    const bool up0 = (y0 + a[NC - 1] * d0) > mx[0], up1 = (y1 + a[NC - 1] * d1) > mx[0];
+    if (__any_sync(__activemask(), up0 || up1)) {
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        const double t0 = y0 + a[j] * d0, t1 = y1 + a[j] * d1;
+        if (up0 && t0 > mx[j]) mx[j] = t0;
+        if (up1 && t1 > mx[j]) mx[j] = t1;
+      }
+    }
+  }
   __device__ __forceinline__ void operator()(double y, double d, double u, int64_t = 0) {
-    double em = mwu_expm1(ea0 * d), emd = 0.0;
-    if (PT == PT_GRID || PT == PT_G16) emd = mwu_expm1(ead * d);
+    double em = xm1(ea0 * d), emd = 0.0;
+    if (PT == PT_GRID || PT == PT_G16) emd = xm1(ead * d);
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
       if (PT == PT_DOUBLE) {
@@ -1057,6 +1096,7 @@ struct PRowFast {
 
 template <int PT, int NC, bool SQ1>
 struct CRowFast {
+  static constexpr double kAbsent = INFINITY;      // z of an absent row
   double a[NC], ea0, ead;
   int sq[NC];
   double ec[NC], tc[NC], mn[NC];
@@ -1139,6 +1179,11 @@ struct CRowFast {
 
 // Generic per-row bodies (any candidate list and modes: fixed steps, exact-shift re-passes).
 struct PRowGen {
+  static constexpr double kAbsent = -INFINITY;
+  __device__ __forceinline__ void pair(double y0, double d0, double u0, double y1, double d1, double u1) {
+    (*this)(y0, d0, u0);
+    if (u1 != 0.0 || y1 != -INFINITY) (*this)(y1, d1, u1);
+  }
   const Cands& k;
   double eta;
   double ep[MWU_MAXC], lp[MWU_MAXC], mx[MWU_MAXC];
@@ -1168,6 +1213,7 @@ struct PRowGen {
 };
 
 struct CRowGen {
+  static constexpr double kAbsent = INFINITY;
   __device__ __forceinline__ void pair(double z0, double d0, double v0, double z1, double d1, double v1) {
     (*this)(z0, d0, v0);
     if (v1 != 0.0 || z1 != INFINITY) (*this)(z1, d1, v1);
