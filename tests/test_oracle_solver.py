@@ -211,3 +211,35 @@ def test_step_counts_standard_vs_search():
         pass
     assert p_bin.status == p_std.status == O.FEASIBLE
     assert p_bin.t * 10 < p_std.t
+
+
+def test_iter_limit_counts_as_infeasible_in_the_outer_search():
+    """Q14: a probe that reaches max_iter is ITER_LIMIT (Alg. 2's loop run for at
+    most max_iter iterations), and the outer geometric bisection treats it as
+    infeasible: the packing search (maximise) then lowers its upper end, the covering
+    search (minimise) raises its lower end.  With max_iter = 1 most probes cannot finish; the
+    recorded probe sequence is replayed against the bisection rule with ITER_LIMIT as infeasible,
+    and the returned witnesses still satisfy the LP."""
+    G = gg.erdos_renyi(60, 240, seed=3)
+    s, d = G.numpy()
+    P = O.incidence_M(s, d, G.n_vertices)
+    L, H, _ = O.packing_bracket(P, 0.1)
+    p = O.run_probe(O.packing_lp(P, math.sqrt(L * H)), 0.1, max_iter=1)
+    assert p.status == O.ITER_LIMIT and p.t == 1
+    C = P.T.tocsr()
+    Lc, Hc, _ = O.covering_bracket(C)
+    for kind, eps, lo, hi, sense in (("match", 0.1, L, H, +1), ("vcover", 0.05, Lc, Hc, -1)):
+        r = O.solve(kind, s, d, G.n_vertices, eps=eps, max_iter=1)
+        assert any(q[1] == O.ITER_LIMIT for q in r.probes)
+        for B, status, t, _ in r.probes:
+            assert B == math.sqrt(lo * hi) and t <= 1
+            ok = status == O.FEASIBLE                        # ITER_LIMIT: not ok (infeasible)
+            if (ok and sense > 0) or (not ok and sense < 0):
+                lo = B
+            else:
+                hi = B
+        assert r.bound == (lo if sense > 0 else hi)
+        if sense > 0:                                        # Theorem P:737-739: P x <= (1 + eps)
+            assert (P @ r.x).max() <= 1 + eps + 1e-12
+        else:
+            assert (C @ r.x).min() >= 1 - 1e-12
