@@ -18,12 +18,14 @@ ap.add_argument("--use-graph", type=int, default=0)
 ap.add_argument("--active", type=int, default=1)
 ap.add_argument("--phases", type=int, default=0)
 ap.add_argument("--bound", type=float, default=0.0, help="probe bound (default: the first outer bisection bound)")
+ap.add_argument("--block-r", type=int, default=0)
 ap.add_argument("--skip", type=int, default=0, help="iterations run through the probe graph before the listed ones")
 a = ap.parse_args()
 kind, eps, _ = bench.WORKLOADS[a.workload]
 G = gg.config_graph(a.workload, scale_down=a.scale_down, seed=1, device="cuda")
 gs = bench.graph_stats(G)
-S = Solver.graph(kind, G.src, G.dst, G.n_vertices, G.n_left if kind == "bmatch" else 0, use_graph=a.use_graph)
+S = Solver.graph(kind, G.src, G.dst, G.n_vertices, G.n_left if kind == "bmatch" else 0, use_graph=a.use_graph,
+                 block_r=a.block_r)
 L, H, _ = bench.bracket(kind, gs, eps)
 B = a.bound if a.bound > 0 else math.sqrt(L * H)
 S.probe_begin(B, eps)
