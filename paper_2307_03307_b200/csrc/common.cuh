@@ -173,6 +173,42 @@ __device__ __forceinline__ void block_partials(const double (&v)[NS], const int*
   __syncthreads();   // sh may be reused by the next call
 }
 
+// block_partials with one compile-time op for all NS slots (the search pass reduces 50 slots per
+// block: with run-time ops the op switch around every shuffle round was ~40% of a small pass's
+// stall samples).  Same per-slot shuffle tree and warp order as block_partials; the NS trees are
+// interleaved.  slot1 >= 0: the partials are also written there.
+template <int OP>
+__device__ __forceinline__ double red_combine_c(double a, double b) {
+  return OP == OP_SUM ? __dadd_rn(a, b) : (OP == OP_MAX ? fmax(a, b) : fmin(a, b));
+}
+template <int NS, int OP>
+__device__ __forceinline__ void block_partials_op(const double (&v)[NS], double* part, int slot0, int slot1 = -1) {
+  __shared__ double sh[MWU_NT / 32][NS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double a[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) a[s] = v[s];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) a[s] = red_combine_c<OP>(a[s], __shfl_down_sync(0xffffffffu, a[s], o));
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) sh[warp][s] = a[s];
+  }
+  __syncthreads();
+  if (threadIdx.x < NS) {
+    const int s = threadIdx.x;
+    double r = sh[0][s];
+#pragma unroll
+    for (int w = 1; w < MWU_NT / 32; ++w) r = red_combine_c<OP>(r, sh[w][s]);
+    part[(size_t)blockIdx.x * MWU_SLOTS + slot0 + s] = r;
+    if (slot1 >= 0) part[(size_t)blockIdx.x * MWU_SLOTS + slot1 + s] = r;
+  }
+  __syncthreads();   // sh may be reused by the next call
+}
+
 // Returns true in the last block to finish; there res[0..nslots) (shared memory) holds the grid
 // result of every slot, combined over blocks 0..gridDim.x-1 in a fixed order.  Must be called
 // by all threads; ops[s] is the op of slot s.
@@ -192,9 +228,22 @@ __device__ __forceinline__ bool last_block_combine(const int* ops, int nslots, c
   const int L = MWU_NT / nslots;          // lanes per slot
   const int s = threadIdx.x % nslots, k = threadIdx.x / nslots;
   double a = red_identity(ops[s]);
-  if (k < L)
-    for (unsigned int b = k; b < gridDim.x; b += L)
-      a = red_combine(ops[s], a, __ldcg(part + (size_t)b * MWU_SLOTS + s));
+  if (k < L) {
+    // same combination order as a plain loop over b = k, k + L, ...; the loads of 8 partials are
+    // issued together (a serial chain of L2 round trips was most of a small kernel's tail)
+    constexpr int UB = 8;
+    for (unsigned int b = k; b < gridDim.x; b += UB * L) {
+      double t[UB];
+#pragma unroll
+      for (int i = 0; i < UB; ++i) {
+        const unsigned int bb = b + i * L;
+        t[i] = bb < gridDim.x ? __ldcg(part + (size_t)bb * MWU_SLOTS + s) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < UB; ++i)
+        if (b + i * L < gridDim.x) a = red_combine(ops[s], a, t[i]);
+    }
+  }
   sh2[threadIdx.x] = a;
   __syncthreads();
   if (threadIdx.x < nslots) {

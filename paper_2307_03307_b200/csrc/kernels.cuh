@@ -20,8 +20,11 @@
 #ifndef MWU_SEARCH_PTAB
 #define MWU_SEARCH_PTAB 0     // packing side of the search: degree-14 Taylor expm1 (1: table-driven,
 #endif                        // as fast but moved the densest-bu310 solve to 2.3% from the oracle's count
-#ifndef MWU_CSR_V4
-#define MWU_CSR_V4 1          // csr_scatter: 16-byte loads of row / column ids (c3 1.70 -> 1.60 ms per iteration)
+#ifndef MWU_CSR_GRID
+#define MWU_CSR_GRID 4        // csr_scatter CTAs per SM (grid-stride, ids of the next chunk prefetched; 8 measured 4% slower)
+#endif
+#ifndef MWU_VC_GRID
+#define MWU_VC_GRID 4         // vc_scatter CTAs per SM
 #endif
 #ifndef MWU_SEARCH_TAB
 #define MWU_SEARCH_TAB 1      // covering side of the search: table-driven (expm1, exp) pair
@@ -1318,17 +1321,12 @@ __device__ __forceinline__ void search_body_fast(const SearchArgs& A, const Cand
                                                  uint64_t* bars, double* part,
                                                  const double* tab) {
   uint32_t it = 0;
-  const int opsS[NC] = {};   // all OP_SUM (0)
-  int opsX[NC], opsN[NC];
-#pragma unroll
-  for (int j = 0; j < NC; ++j) { opsX[j] = OP_MAX; opsN[j] = OP_MIN; }
   {
     PRowFast<PT, NC, SQ1> f(K, c->eta, tab);
     if (!c->pSing) stream_rows3(A.y, A.dy, A.u, A.mP, sbuf, bars, it, f);
     if (!c->pSing && A.mP2 > 0) stream_rows3(A.y2, A.dy2, A.u2, A.mP2, sbuf, bars, it, f);
-    block_partials<NC>(f.ep, opsS, part, R_EP(0));
-    block_partials<NC>(f.ep, opsS, part, R_LP(0));          // LSE-mode candidates read this slot
-    block_partials<NC>(f.mx, opsX, part, R_MX(0));
+    block_partials_op<NC, OP_SUM>(f.ep, part, R_EP(0), R_LP(0));   // LSE-mode candidates read R_LP
+    block_partials_op<NC, OP_MAX>(f.mx, part, R_MX(0));
   }
   {
     CRowFast<PT, NC, SQ1> f(K, tab);
@@ -1336,30 +1334,25 @@ __device__ __forceinline__ void search_body_fast(const SearchArgs& A, const Cand
       if (A.rz) stream_recs3(A.rz, A.rdz, A.rv, A.tcnt, A.nstreams, A.rcap, sbuf, bars, it, f);
       else stream_rows3(A.z, A.dz, A.v, A.mC, sbuf, bars, it, f);
     }
-    block_partials<NC>(f.ec, opsS, part, R_EC(0));
-    block_partials<NC>(f.tc, opsS, part, R_TC(0));
-    block_partials<NC>(f.mn, opsN, part, R_MN(0));
+    block_partials_op<NC, OP_SUM>(f.ec, part, R_EC(0));
+    block_partials_op<NC, OP_SUM>(f.tc, part, R_TC(0));
+    block_partials_op<NC, OP_MIN>(f.mn, part, R_MN(0));
   }
-  const double zero2[2] = {0.0, 0.0};
-  const int ops2[2] = {OP_SUM, OP_SUM};
-  block_partials<2>(zero2, ops2, part, R_NP);
+  if (threadIdx.x < 2) part[(size_t)blockIdx.x * MWU_SLOTS + R_NP + threadIdx.x] = 0.0;   // no Newton sums
 }
 
 __device__ __forceinline__ void search_body_gen(const SearchArgs& A, const Cands& K, const Ctl* c, double* sbuf,
                                                 uint64_t* bars, double* part) {
   uint32_t it = 0;
-  int opsS[MWU_MAXC], opsX[MWU_MAXC], opsN[MWU_MAXC];
-#pragma unroll
-  for (int j = 0; j < MWU_MAXC; ++j) { opsS[j] = OP_SUM; opsX[j] = OP_MAX; opsN[j] = OP_MIN; }
   double nd[2] = {0.0, 0.0};           // Newton derivative sums (P side, C side)
   {
     PRowGen f(K, c->eta);
     if (!c->pSing) stream_rows3(A.y, A.dy, A.u, A.mP, sbuf, bars, it, f);
     if (!c->pSing && A.mP2 > 0) stream_rows3(A.y2, A.dy2, A.u2, A.mP2, sbuf, bars, it, f);
     nd[0] = f.nd;
-    block_partials<MWU_MAXC>(f.ep, opsS, part, R_EP(0));
-    block_partials<MWU_MAXC>(f.lp, opsS, part, R_LP(0));
-    block_partials<MWU_MAXC>(f.mx, opsX, part, R_MX(0));
+    block_partials_op<MWU_MAXC, OP_SUM>(f.ep, part, R_EP(0));
+    block_partials_op<MWU_MAXC, OP_SUM>(f.lp, part, R_LP(0));
+    block_partials_op<MWU_MAXC, OP_MAX>(f.mx, part, R_MX(0));
   }
   {
     CRowGen f(K, -c->eta);
@@ -1367,12 +1360,12 @@ __device__ __forceinline__ void search_body_gen(const SearchArgs& A, const Cands
       if (A.rz) stream_recs3(A.rz, A.rdz, A.rv, A.tcnt, A.nstreams, A.rcap, sbuf, bars, it, f);
       else stream_rows3(A.z, A.dz, A.v, A.mC, sbuf, bars, it, f);
     }
-    block_partials<MWU_MAXC>(f.ec, opsS, part, R_EC(0));
-    block_partials<MWU_MAXC>(f.tc, opsS, part, R_TC(0));
-    block_partials<MWU_MAXC>(f.mn, opsN, part, R_MN(0));
+    block_partials_op<MWU_MAXC, OP_SUM>(f.ec, part, R_EC(0));
+    block_partials_op<MWU_MAXC, OP_SUM>(f.tc, part, R_TC(0));
+    block_partials_op<MWU_MAXC, OP_MIN>(f.mn, part, R_MN(0));
     nd[1] = f.nd;
   }
-  block_partials<2>(nd, opsS, part, R_NP);
+  block_partials_op<2, OP_SUM>(nd, part, R_NP);
 }
 
 // One HBM pass evaluating the staged candidates (P:716-727 on cached vectors); the
@@ -1955,29 +1948,38 @@ __global__ void __launch_bounds__(MWU_NT) csr_scatter(int64_t nnz, const int32_t
   constexpr int U = 4;
   const int lane = threadIdx.x & 31;
   const int64_t chunk = (int64_t)U * MWU_NT;
-  for (int64_t base = (int64_t)blockIdx.x * chunk; base < nnz; base += (int64_t)gridDim.x * chunk) {
-    const int64_t q0 = base + (int64_t)threadIdx.x * U;
-    int r[U];
-    double val[U];
-#if MWU_CSR_V4
-    if (q0 + U <= nnz && (((uintptr_t)(rowid + q0) | (uintptr_t)(col + q0)) & 15) == 0) {
-      // 16-byte loads of the 4 row ids and column ids (one instruction each)
-      const int4 rr = __ldcs(reinterpret_cast<const int4*>(rowid + q0));
-      const uint4 cc = __ldcs(reinterpret_cast<const uint4*>(col + q0));
-      r[0] = rr.x; r[1] = rr.y; r[2] = rr.z; r[3] = rr.w;
-      val[0] = __ldg(w + cc.x); val[1] = __ldg(w + cc.y); val[2] = __ldg(w + cc.z); val[3] = __ldg(w + cc.w);
+  const bool al16 = (((uintptr_t)rowid | (uintptr_t)col) & 15) == 0;      // q0 is a multiple of 4
+  // row / column ids of the 4 nonzeros at q0 (16-byte loads where aligned and in range)
+  auto load_ids = [&](int64_t q0, int (&rr)[U], uint32_t (&cc)[U]) {
+    if (q0 + U <= nnz && al16) {
+      const int4 a = __ldcs(reinterpret_cast<const int4*>(rowid + q0));
+      const uint4 b = __ldcs(reinterpret_cast<const uint4*>(col + q0));
+      rr[0] = a.x; rr[1] = a.y; rr[2] = a.z; rr[3] = a.w;
+      cc[0] = b.x; cc[1] = b.y; cc[2] = b.z; cc[3] = b.w;
     } else {
 #pragma unroll
-      for (int k = 0; k < U; ++k) r[k] = (q0 + k < nnz) ? __ldcs(rowid + q0 + k) : -1;
-#pragma unroll
-      for (int k = 0; k < U; ++k) val[k] = (r[k] >= 0) ? __ldg(w + __ldcs(col + q0 + k)) : 0.0;
+      for (int k = 0; k < U; ++k) {
+        const bool in = q0 + k < nnz;
+        rr[k] = in ? __ldcs(rowid + q0 + k) : -1;
+        cc[k] = in ? __ldcs(col + q0 + k) : 0u;
+      }
     }
-#else
+  };
+  int rn[U];
+  uint32_t cn[U];
+  const int64_t stride = (int64_t)gridDim.x * chunk;
+  int64_t base = (int64_t)blockIdx.x * chunk;
+  if (base < nnz) load_ids(base + (int64_t)threadIdx.x * U, rn, cn);
+  for (; base < nnz; base += stride) {
+    int r[U];
+    uint32_t ci[U];
+    double val[U];
 #pragma unroll
-    for (int k = 0; k < U; ++k) r[k] = (q0 + k < nnz) ? __ldcs(rowid + q0 + k) : -1;
+    for (int k = 0; k < U; ++k) { r[k] = rn[k]; ci[k] = cn[k]; }
+    // ids of the next chunk are requested before this chunk's gathers (two chunks in flight)
+    if (base + stride < nnz) load_ids(base + stride + (int64_t)threadIdx.x * U, rn, cn);
 #pragma unroll
-    for (int k = 0; k < U; ++k) val[k] = (r[k] >= 0) ? __ldg(w + __ldcs(col + q0 + k)) : 0.0;
-#endif
+    for (int k = 0; k < U; ++k) val[k] = (r[k] >= 0) ? __ldg(w + ci[k]) : 0.0;
     // out-of-range entries (r = -1) only occur at the end, after every valid one
     const int kh = r[0], kt = r[U - 1];
     double head = 0.0, tail = 0.0;

@@ -981,10 +981,10 @@ void enqueue_column(mwu_ctx* c, cudaStream_t st) {
       if (c->fastC) {
         CK(cudaMemsetAsync(c->hsum, 0, c->n * sizeof(double), st));
         if (c->kind == K_VCOVER)
-          vc_scatter<<<(int)std::min<int64_t>(4 * c->sms, (c->E + 4 * MWU_NT - 1) / (4 * MWU_NT) + 1), MWU_NT, 0, st>>>(
+          vc_scatter<<<(int)std::min<int64_t>(MWU_VC_GRID * c->sms, (c->E + 4 * MWU_NT - 1) / (4 * MWU_NT) + 1), MWU_NT, 0, st>>>(
               c->E, c->src, c->dst, c->v, c->hsum, c->ctl);
         else if (!c->sharded)
-          csr_scatter<<<(int)std::min<int64_t>(4 * c->sms, (c->nnzC + 4 * MWU_NT - 1) / (4 * MWU_NT) + 1), MWU_NT, 0, st>>>(
+          csr_scatter<<<(int)std::min<int64_t>(MWU_CSR_GRID * c->sms, (c->nnzC + 4 * MWU_NT - 1) / (4 * MWU_NT) + 1), MWU_NT, 0, st>>>(
               c->nnzC, c->rowidC, c->csrC.idx, c->v, c->hsum, c->ctl, 0);
         else   // local rows: C^T v by scattering each local row's weight to its columns (C symmetric)
           csr_scatter_T<<<(int)std::min<int64_t>(4 * c->sms, (c->nnzL + 4 * MWU_NT - 1) / (4 * MWU_NT) + 1), MWU_NT, 0, st>>>(
@@ -1069,7 +1069,7 @@ void enqueue_forward(mwu_ctx* c, cudaStream_t st, const double* in, double* oy, 
       if (c->fastC) {
         CK(cudaMemsetAsync(oz, 0, (c->mC > 0 ? c->mC : 1) * sizeof(double), st));
         const int64_t nz = c->sharded ? c->nnzL : c->nnzC;
-        csr_scatter<<<(int)std::min<int64_t>(4 * c->sms, (nz + 4 * MWU_NT - 1) / (4 * MWU_NT) + 1), MWU_NT, 0, st>>>(
+        csr_scatter<<<(int)std::min<int64_t>(MWU_CSR_GRID * c->sms, (nz + 4 * MWU_NT - 1) / (4 * MWU_NT) + 1), MWU_NT, 0, st>>>(
             nz, c->rowidC + c->k0, c->csrC.idx + c->k0, in, oz, c->ctl, c->r0);
         c->launches++;
         if (!init && c->compC) {
