@@ -1,8 +1,10 @@
 """Multi-GPU layer: edge-sharded iteration with one allreduce of the
 scattered forward product per iteration plus allgathered phase reductions.
 
-CPU (`-m "not gpu"`): the shard ranges tile the edge list, and the unique-id distribution over a
-world-size-2 gloo group (the same code path graph_distributed uses with NCCL).
+CPU (`-m "not gpu"`): the shard ranges tile the edge list, the unique-id distribution over a
+world-size-2 gloo group (the same code path graph_distributed uses with NCCL), and the two exchange
+patterns (edge-sharded forward product, row-sharded transposed product: partial scatter + one
+allreduce) over that group against the oracle's incidence product.
 GPU: the sharded engine with an in-process rank group on one device (SimGroup: one host thread
 per rank, host barriers, no kernel waits on another) against the single-GPU engine and the
 oracle: fixed-step vectors within 1e-10 relative, identical searched solves."""
@@ -67,6 +69,50 @@ def test_unique_id_and_ranges_over_gloo():
     ranges = res[0][1]
     assert ranges == res[1][1]
     assert ranges[0][0] == 0 and ranges[-1][1] == E and ranges[0][1] == ranges[1][0]
+
+
+def _gloo_exchange_worker(rank, world, port, out):
+    """The sharded engine's two exchange patterns over a real process group: the
+    edge-sharded matching forward product d^(y) = M d (each rank scatters its mwu_shard_range of
+    the edges, one allreduce of the row vector), and the row-sharded vertex-cover transposed
+    product h = M w (each rank's covering rows, one allreduce of the length-n gradient)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2307_03307_b200 import mwu
+    G = gg.bipartite_zipf(700, 900, 5003, seed=4)              # same seeded graph on every rank
+    src, dst = G.src.numpy().astype(np.int64), G.dst.numpy().astype(np.int64)
+    E, n = len(src), G.n_vertices
+    rng = np.random.default_rng(11)
+    d = rng.random(E)                                          # one value per edge (variable / covering row)
+    e0, e1 = mwu.shard_range(E, world, rank)
+    part = np.zeros(n)
+    np.add.at(part, src[e0:e1], d[e0:e1])
+    np.add.at(part, dst[e0:e1], d[e0:e1])
+    t = torch.from_numpy(part)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    cnt = torch.tensor([e1 - e0], dtype=torch.int64)
+    dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+    out[rank] = (t.numpy().copy(), int(cnt.item()), (e0, e1))
+    dist.destroy_process_group()
+
+
+def test_sharded_products_over_gloo():
+    world = 2
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_gloo_exchange_worker, args=(world, port, out), nprocs=world, join=True)
+        res = dict(out)
+    G = gg.bipartite_zipf(700, 900, 5003, seed=4)
+    src, dst = G.src.numpy(), G.dst.numpy()
+    M = O.incidence_M(src, dst, G.n_vertices)                  # vertices x edges (P:941-956)
+    d = np.random.default_rng(11).random(len(src))
+    want = O.matvec(M, d)
+    assert res[0][1] == res[1][1] == len(src)                   # the ranges cover every edge once
+    assert res[0][2][1] == res[1][2][0]
+    for r in range(world):
+        np.testing.assert_allclose(res[r][0], want, rtol=1e-13, atol=0)
+    np.testing.assert_array_equal(res[0][0], res[1][0])         # every rank holds the same reduced vector
 
 
 # ---------------------------------------------------------------------------------- GPU
