@@ -33,6 +33,11 @@ WELL_CONDITIONED = {
 }
 
 
+# Instances whose iteration count the default (atomically reduced) engine does not reproduce from
+# run to run within +-2% (measured: tools/rerun_bu310.py); their count is asserted on the
+# fixed-order engine (tests/test_gpu_parity.py::test_full_solve_parity).
+FIXED_ORDER_COUNT = {"densest-bu310"}
+
 NOISE = 2.0 ** -49   # 8 ulps per iteration and summed term, as tests/gpu_common.self_drift
 
 

@@ -79,7 +79,7 @@ keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
-        "launch__registers_per_thread", "smsp__inst_executed.sum"]
+        "launch__registers_per_thread", "launch__grid_size", "smsp__inst_executed.sum"]
 for w in ("c4", "c5", "c2", "c3"):
     rawp = os.path.join(G, f"prof_r2_{w}_raw.csv")
     if not os.path.exists(rawp):
@@ -88,8 +88,10 @@ for w in ("c4", "c5", "c2", "c3"):
     if not rr:
         continue
     hh = rr[0]
-    lines = [f"ncu --set full --clock-control none --import-source on (tools/evidence_r2.sh) python tools/diag.py "
-             f"--workload {w} --iters 12 --active 0   ({w}, first probe, iterations ~10; round 2, {tag})", ""]
+    skip = {"c4": "-s 40 -c 3", "c2": "-s 16 -c 8", "c3": "-s 2 -c 8", "c5": "-s 30 -c 3"}[w]
+    lines = [f"ncu --set full --clock-control none --import-source on {skip} (tools/evidence_r2f.sh; -s/-c of earlier "
+             f"tags: tools/evidence_r2.sh) python tools/diag.py --workload {w} --iters 12 --active 0   "
+             f"({w}, first probe, host-driven iterations; round 2, {tag})", ""]
     for r in rr[2:]:
         d = dict(zip(hh, r))
         lines.append(d.get("Kernel Name", "?").split("(")[0])
